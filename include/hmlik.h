@@ -1,0 +1,171 @@
+/*
+ * hmlik.h -- C-ABI of the B200-native H-matrix Gaussian log-likelihood library.
+ *
+ * The hot path of PAPER.md, "Likelihood Approximation
+ * With Hierarchical Matrices For Large Spatial Datasets":
+ *
+ *   L(theta) = -n/2 log(2 pi) - 1/2 log det C(theta) - 1/2 Z^T C(theta)^{-1} Z     Eq. (1), l.52-55
+ *   C(h; theta) = sigma^2 / (2^(nu-1) Gamma(nu)) (h/ell)^nu K_nu(h/ell)             Eq. (2), l.183-188
+ *   L~(theta) = -n/2 log(2 pi) - sum_i log L~_ii - 1/2 v^T v,  L~ v = Z              Eq. (4), l.259-265
+ *
+ * with C(theta) held in H-matrix format (sec. 2.1, Definition 1, l.152-160): a
+ * geometric cluster tree over the n locations, a block cluster tree split by
+ * the admissibility condition, admissible blocks compressed to relative
+ * accuracy eps by ACA (l.147) + QR/SVD recompression (sec. 1 item 6, l.87),
+ * an H-Cholesky factorisation with truncated low-rank updates (l.281-283),
+ * log det = 2 sum log diag(L~) (l.283) and a forward solve for the quadratic
+ * form (l.265).  DESIGN.md lists every reading of the paper this library takes.
+ *
+ * Conventions for every entry point
+ *  - All floating point is IEEE fp64.  Locations are n x 2 row-major
+ *    (x0, y0, x1, y1, ...).  Vectors/matrices of data (Z, xi, outputs) are
+ *    column-major n x k (column j = replicate j) in the ORIGINAL location order.
+ *  - A pointer argument documented "host or device" is interpreted according to
+ *    the accompanying `*_on_device` flag (0 = host memory, 1 = device memory of
+ *    the handle's CUDA device).  Host buffers are copied synchronously through
+ *    pinned staging; device buffers are used in place on the handle's stream.
+ *  - Ownership: the library never takes ownership of caller memory and never
+ *    frees it.  Handles are created by hm_build / hm_tree_build and released by
+ *    hm_free / hm_tree_free.
+ *  - Errors: every function returns an int status (HM_OK = 0 on success, a
+ *    negative HM_ERR_* code otherwise) and never aborts the process.  A
+ *    human-readable message for the last error on the calling thread is
+ *    available from hm_last_error().  No function falls back to a CPU path:
+ *    without a usable CUDA device, GPU entry points return HM_ERR_CUDA.
+ *  - Thread-safety: a handle may be used by one thread at a time.
+ */
+#ifndef HMLIK_H
+#define HMLIK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define HM_OK               0
+#define HM_ERR_ARG         -1   /* invalid argument (sizes, NaN, theta <= 0, ...)        */
+#define HM_ERR_CUDA        -2   /* CUDA runtime error / no device                         */
+#define HM_ERR_NOT_SPD     -3   /* Cholesky pivot <= 0 (factor not positive definite)     */
+#define HM_ERR_RANK_CAP    -4   /* a truncation needed more rank than the block capacity  */
+#define HM_ERR_OOM         -5   /* device or host allocation failed                        */
+#define HM_ERR_STATE       -6   /* call order violated (e.g. loglik before cholesky)       */
+#define HM_ERR_TOO_LARGE   -7   /* n above the dense check-path cap                        */
+
+/* theta = (sigma^2, ell, nu), all > 0 (Eq. 2; sec. 2.2 l.187).                  */
+typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
+
+/* H-matrix parameters.  eps: relative accuracy per admissible block (Remark 2,
+ * l.166, adaptive-rank strategy; reading R4); leaf: n_min (l.211);
+ * eta: admissibility parameter (reading R2); kmax: rank capacity of one
+ * low-rank block (HM_ERR_RANK_CAP when exceeded; 0 = default 160).            */
+typedef struct hm_params {
+    double  eps;
+    int32_t leaf;
+    double  eta;
+    int32_t kmax;
+} hm_params;
+
+typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */
+typedef struct hm_tree_s*   hm_tree;            /* geometry only (host)              */
+
+/* ---- error reporting --------------------------------------------------- */
+const char* hm_last_error(void);
+/* Library version string. */
+const char* hm_version(void);
+
+/* ---- geometry: cluster tree + block cluster tree (host, no GPU) --------- */
+/* Build the cluster tree T_I (median bisection along the longest bounding-box
+ * axis, reading R1) and the block cluster tree T_{IxI} (reading R2/R3) for n
+ * host locations.  Errors: HM_ERR_ARG for n < 1, leaf < 1, eta <= 0 or a
+ * non-finite coordinate.                                                   */
+int hm_tree_build(const double* locs_host, int64_t n, int32_t leaf, double eta, hm_tree* out);
+int hm_tree_free(hm_tree t);
+/* counts[0..5] = n, #clusters, #leaf clusters, depth, #leaf blocks (full I x I),
+ *                #admissible leaf blocks (full I x I).                        */
+int hm_tree_counts(hm_tree t, int64_t counts[6]);
+/* perm[k] = original index of the k-th point in tree order (n entries).      */
+int hm_tree_perm(hm_tree t, int64_t* perm_host);
+/* Clusters in pre-order: 4 int64 per cluster (lo, hi, level, is_leaf).      */
+int hm_tree_clusters(hm_tree t, int64_t* out_host);
+/* Leaf blocks of the FULL partition of I x I, 6 int64 per block
+ * (t_lo, t_hi, s_lo, s_hi, level, admissible), in recursion order.          */
+int hm_tree_blocks(hm_tree t, int64_t* out_host);
+
+/* Diagnostics (host only): build the H-Cholesky / solve plan for the tree
+ * with rank capacity kmax and write it to the binary file `path` (sections
+ * of int64 count + raw task structs, see tests/plan_interp.py), or, if path
+ * is NULL, only fill summary[0..7] = pool doubles, #slots, #chol VM tasks,
+ * #chol truncation tasks, #chol waves, #chol launches, #solve waves,
+ * #solve tasks.  HM_ERR_ARG for unsupported geometry.                       */
+int hm_plan_dump(hm_tree t, int32_t kmax, const char* path, double summary[8]);
+
+/* ---- H-matrix likelihood (GPU) ------------------------------------------ */
+/* hm_build(locs, theta, eps, leaf, eta): build geometry, plan the H-Cholesky,
+ * allocate device storage and assemble C~(theta) (Matern blocks with device
+ * K_nu, ACA + recompression of admissible blocks).  locs: n x 2, host or
+ * device (locs_on_device).  stream: cudaStream_t to run on (NULL = the
+ * library's own stream).  device: CUDA ordinal.                             */
+int hm_build(const double* locs, int32_t locs_on_device, int64_t n,
+             hm_theta theta, hm_params params, int32_t device, void* stream,
+             hm_handle* out);
+int hm_free(hm_handle h);
+
+/* Re-assemble C~(theta) for a new theta on the same locations (same tree,
+ * same plan).                                                                */
+int hm_assemble(hm_handle h, hm_theta theta);
+
+/* H-Cholesky C~ = L~ L~^T in place with truncated low-rank updates (relative
+ * accuracy params.eps).  HM_ERR_NOT_SPD if a pivot is not positive.          */
+int hm_cholesky(hm_handle h);
+
+/* Log-likelihood Eq. (4) for k data vectors Z (n x k column-major, original
+ * order, host or device).  out[3*j + 0..2] = (loglik, logdet, quad) of column
+ * j, written to host memory.  Requires hm_cholesky first (HM_ERR_STATE).    */
+int hm_loglik(hm_handle h, const double* Z, int32_t z_on_device, int32_t k, double* out_host);
+
+/* One full evaluation per theta: for each of n_theta thetas, assemble +
+ * Cholesky + loglik for the k columns of Z.  out: n_theta x k x 3 (host).
+ * Failed factorizations store (-inf, nan, nan) for that theta and continue;
+ * the return value is the first error seen (HM_OK if none).                 */
+int hm_loglik_batch(hm_handle h, const hm_theta* thetas_host, int32_t n_theta,
+                    const double* Z, int32_t z_on_device, int32_t k, double* out_host);
+
+/* Sampler (sec. 4, l.308 "Z = L~ xi"): Z = L~ xi for k standard-normal
+ * columns xi (n x k, original order, host or device); Z written in original
+ * order to host or device memory.  Requires hm_cholesky first.              */
+int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k,
+              double* Z, int32_t z_on_device);
+
+/* y = C~ x (H-matrix times k vectors; Table 1 row "C~ z").  Valid after
+ * hm_build/hm_assemble and before hm_cholesky (which overwrites C~).        */
+int hm_matvec(hm_handle h, const double* x, int32_t x_on_device, int32_t k,
+              double* y, int32_t y_on_device);
+
+/* Statistics.  st[0..11]: n, #dense blocks, #low-rank blocks, max rank C~,
+ * max rank L~, bytes C~, bytes L~, compression ratio C~ (1 - bytes/8n^2),
+ * #plan tasks, #plan waves, #kernel launches per Cholesky, rank-cap flag.   */
+int hm_stats(hm_handle h, double st[12]);
+
+/* Timing of the last hm_assemble / hm_cholesky / hm_loglik on the device,
+ * milliseconds (CUDA events on the handle's stream): ms[0..2].              */
+int hm_timings(hm_handle h, double ms[3]);
+
+/* ---- dense fp64 check path (n <= 16384) --------------------------------- */
+/* Exact Eq. (1) on the GPU with dense Matern assembly, dense blocked
+ * Cholesky, log det and forward solve; out[3*j+0..2] as in hm_loglik.
+ * HM_ERR_TOO_LARGE for n > 16384.                                          */
+int hm_dense_loglik(const double* locs, int32_t locs_on_device, int64_t n, hm_theta theta,
+                    const double* Z, int32_t z_on_device, int32_t k,
+                    int32_t device, void* stream, double* out_host);
+
+/* Dense Matern covariance block on the GPU (test hook for the device K_nu):
+ * out[i + j*ni] = C(|a_i - b_j|; theta), a: ni x 2, b: nj x 2, host arrays.  */
+int hm_matern_block(const double* a_host, int64_t ni, const double* b_host, int64_t nj,
+                    hm_theta theta, int32_t device, double* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HMLIK_H */

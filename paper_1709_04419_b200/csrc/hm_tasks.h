@@ -1,0 +1,80 @@
+// Task formats shared by the host planner (plan.cpp) and the device kernels
+// (hm_kernels.cu).  Plain POD structs, 8-byte aligned, copied to device once
+// per plan.  All offsets are in doubles into the handle's device pool.
+#pragma once
+#include <cstdint>
+
+namespace hm {
+
+// ---- tile VM -------------------------------------------------------------
+// One CTA executes a short program on NTILE 64 x 64 fp64 shared-memory tiles.
+enum VmOp : uint8_t {
+    VM_LD = 1,       // tile[t0] <- pool[goff] (rows x cols, ld), zero padded
+    VM_ST = 2,       // pool[goff] <- tile[t0] (its rows x cols)
+    VM_GEMM = 3,     // tile[t0] = beta*tile[t0] + alpha*op(tile[t1]) op(tile[t2])
+    VM_POTRF = 4,    // tile[t0] <- chol(tile[t0]); sum log diag -> pool[goff]; fail -> flags[0]
+    VM_TRSM_RLT = 5, // tile[t0] <- tile[t0] tile[t1]^{-T}
+    VM_TRSM_LN = 6,  // tile[t0] <- tile[t1]^{-1} tile[t0]
+    VM_TRMM_LN = 7,  // tile[t0] <- tile[t1] tile[t0]
+    VM_ZERO = 8,     // tile[t0] <- 0 with dims (rows x cols)
+};
+constexpr int NTILE = 5;
+
+// Dimension spec: actual = (slot < 0) ? stat : clamp(ranks[slot] - off, 0, stat)
+struct Dim {
+    int32_t stat;
+    int32_t slot;
+    int32_t off;
+    int32_t pad;
+};
+
+struct VIns {
+    uint8_t op, t0, t1, t2;
+    uint8_t ta, tb, pad0, pad1;
+    Dim rows, cols;
+    int64_t goff;
+    int32_t ld;
+    int32_t pad2;
+    double alpha, beta;
+};
+
+struct VTask {
+    int32_t ins_begin;
+    int32_t ins_count;
+};
+
+// ---- truncation of an accumulated low-rank sum -------------------------
+// B <- best rank-r approximation (sigma_i > eps * sigma_1) of
+//      sum_p alpha_p * pad(U_p) pad(V_p)^T,   B m x q.
+struct TPiece {
+    int64_t u_off, v_off;
+    int32_t u_ld, v_ld;
+    int32_t u_row0, u_rows;   // placement of U_p rows inside the target's rows
+    int32_t v_row0, v_rows;   // placement of V_p rows inside the target's columns
+    Dim w;                    // width (columns) of the piece
+    double alpha;
+};
+
+struct TTask {
+    int64_t u_out, v_out;     // output U (m x cap, ld m), V (q x cap, ld q)
+    int64_t ws;               // workspace offset (doubles), size ws_size
+    int64_t ws_size;
+    int32_t m, q, cap, rslot;
+    int32_t piece_begin, piece_count;
+    int32_t kmax_tot;         // sum of static piece widths
+    int32_t pad;
+};
+
+// ---- assembly ------------------------------------------------------------
+struct DenseGenTask {         // D[i + j m] = C(|x_{r0+i} - x_{c0+j}|), i < m, j < q
+    int64_t off;
+    int32_t r0, c0, m, q;
+};
+
+struct AcaTask {              // ACA of the m x q block rows [r0, r0+m) x cols [c0, c0+q)
+    int64_t u_off, v_off;     // U m x cap (ld m), V q x cap (ld q)
+    int32_t r0, c0, m, q;
+    int32_t cap, rslot;
+};
+
+}  // namespace hm

@@ -1,0 +1,394 @@
+// H-matrix entry points of include/hmlik.h: hm_build, hm_assemble, hm_cholesky,
+// hm_loglik, hm_loglik_batch, hm_sample, hm_stats, hm_timings.
+//
+// The handle owns: the host tree + plan (built once per location set), one
+// device pool holding every block of C~ / L~ plus all planned temporaries,
+// the device copies of the task lists, and a CUDA stream.  Each phase is a
+// sequence of waves; a wave launches the tile VM for its VM tasks and the
+// truncation kernel for its truncation tasks.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "../../include/hmlik.h"
+#include "api_util.h"
+#include "common.h"
+#include "hm_kernels.h"
+#include "plan.h"
+#include "tree.h"
+
+namespace hm {
+
+struct DPhase {
+    DevBuf ins, vt, tt, tp;
+    const Phase* ph = nullptr;
+};
+
+}  // namespace hm
+
+using namespace hm;
+
+struct hm_handle_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    Tree T;
+    Plan P;
+    hm_params prm{};
+    hm_theta theta{};
+    MaternParams mp{};
+    DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca;
+    DPhase rec, chol, solve, lmul;
+    bool assembled = false, factored = false;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    double ms[3] = {0, 0, 0};
+    int max_rank_C = 0, max_rank_L = 0;
+    std::vector<int> h_ranks;
+    ~hm_handle_s() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+template <class T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+    b.alloc(sizeof(T) * (v.size() + 1));
+    if (!v.empty()) HM_CUDA_TRY(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+}
+
+void upload_phase(DPhase& d, const Phase& p, cudaStream_t st) {
+    upload(d.ins, p.ins, st);
+    upload(d.vt, p.vt, st);
+    upload(d.tt, p.tt, st);
+    upload(d.tp, p.tp, st);
+    d.ph = &p;
+}
+
+void run_phase(hm_handle_s* h, const DPhase& d) {
+    const Phase& p = *d.ph;
+    double* pool = h->pool.as<double>();
+    int* ranks = h->ranks.as<int>();
+    int* flags = h->flags.as<int>();
+    for (int w = 0; w < p.nwaves; ++w) {
+        const int v0 = p.v_wave_begin[w], v1 = p.v_wave_begin[w + 1];
+        const int t0 = p.t_wave_begin[w], t1 = p.t_wave_begin[w + 1];
+        if (t1 > t0)
+            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->prm.eps, h->stream);
+        if (v1 > v0) launch_vm(d.vt.as<VTask>() + v0, v1 - v0, d.ins.as<VIns>(), pool, ranks, flags, h->stream);
+    }
+    HM_CUDA_TRY(cudaGetLastError());
+}
+
+float elapsed(hm_handle_s* h) {
+    float t = 0;
+    HM_CUDA_TRY(cudaEventElapsedTime(&t, h->ev[0], h->ev[1]));
+    return t;
+}
+
+void read_flags(hm_handle_s* h, int f[4]) {
+    HM_CUDA_TRY(cudaMemcpyAsync(f, h->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, h->stream));
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+}
+
+int max_rank(hm_handle_s* h) {
+    h->h_ranks.resize(h->P.n_slots);
+    if (h->P.n_slots == 0) return 0;
+    HM_CUDA_TRY(cudaMemcpyAsync(h->h_ranks.data(), h->ranks.p, sizeof(int) * h->P.n_slots, cudaMemcpyDeviceToHost,
+                                h->stream));
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    int mx = 0;
+    for (int r : h->h_ranks) mx = std::max(mx, r);
+    return mx;
+}
+
+void do_assemble(hm_handle_s* h, hm_theta th) {
+    check_theta(th);
+    h->theta = th;
+    matern_setup(th.sigma2, th.ell, th.nu, h->mp);
+    HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
+    HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+    launch_dense_gen(h->dgen.as<DenseGenTask>(), (int)h->P.dgen.size(), h->pts.as<double>(), h->pool.as<double>(),
+                     h->mp, h->stream);
+    // ACA at eps/4, then recompression to eps (QR + SVD)
+    launch_aca(h->aca.as<AcaTask>(), (int)h->P.aca.size(), h->pts.as<double>(), h->pool.as<double>(),
+               h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->prm.eps, h->stream);
+    run_phase(h, h->rec);
+    HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+    int f[4];
+    read_flags(h, f);
+    h->ms[0] = elapsed(h);
+    h->assembled = true;
+    h->factored = false;
+    h->max_rank_C = max_rank(h);
+    if (f[1]) throw ApiError(HM_ERR_RANK_CAP, "assembly: a block needs more than kmax = " +
+                                                  std::to_string(h->prm.kmax) + " ranks at this eps");
+}
+
+void do_cholesky(hm_handle_s* h) {
+    if (!h->assembled) throw ApiError(HM_ERR_STATE, "hm_cholesky: assemble first");
+    if (h->factored) throw ApiError(HM_ERR_STATE, "hm_cholesky: already factored (re-assemble first)");
+    HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
+    HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+    run_phase(h, h->chol);
+    HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+    int f[4];
+    read_flags(h, f);
+    h->ms[1] = elapsed(h);
+    h->assembled = false;   // C~ has been overwritten by L~
+    if (f[0]) throw ApiError(HM_ERR_NOT_SPD, "H-Cholesky: " + std::to_string(f[0]) + " non-positive pivot(s)");
+    h->factored = true;
+    if (f[1]) throw ApiError(HM_ERR_RANK_CAP, "H-Cholesky: a truncation needed more than kmax ranks");
+}
+
+// Z (n x k, original order, host/device) -> out (k x 3) on host
+void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_host) {
+    if (!h->factored) throw ApiError(HM_ERR_STATE, "hm_loglik: call hm_cholesky first");
+    const int64_t n = h->T.n;
+    const int zw = h->P.zw;
+    double* zt = h->pool.as<double>() + h->P.z_off;
+    HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+    for (int c0 = 0; c0 < k; c0 += zw) {
+        const int kc = std::min(zw, k - c0);
+        const double* src;
+        if (zdev) {
+            src = Z + (int64_t)c0 * n;
+        } else {
+            h->zio.alloc(sizeof(double) * n * zw);
+            HM_CUDA_TRY(cudaMemcpyAsync(h->zio.p, Z + (int64_t)c0 * n, sizeof(double) * n * kc, cudaMemcpyHostToDevice,
+                                        h->stream));
+            src = h->zio.as<double>();
+        }
+        launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+        run_phase(h, h->solve);
+        launch_finish(h->pool.as<double>() + h->P.logd_off, h->P.n_leaves, zt, n, kc, h->out.as<double>(), h->stream);
+        HM_CUDA_TRY(cudaMemcpyAsync(out_host + 3 * c0, h->out.p, sizeof(double) * 3 * kc, cudaMemcpyDeviceToHost,
+                                    h->stream));
+    }
+    HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    h->ms[2] = elapsed(h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta theta, hm_params params, int32_t device,
+             void* stream, hm_handle* out) {
+    hm_handle_s* h = nullptr;
+    try {
+        if (!locs || !out) throw ApiError(HM_ERR_ARG, "null pointer");
+        if (n < 1) throw ApiError(HM_ERR_ARG, "n >= 1 required");
+        if (!(params.eps > 0.0 && params.eps < 1.0)) throw ApiError(HM_ERR_ARG, "0 < eps < 1 required");
+        if (params.leaf < 1 || params.leaf > 64) throw ApiError(HM_ERR_ARG, "1 <= leaf <= 64 required");
+        if (!(params.eta > 0.0)) throw ApiError(HM_ERR_ARG, "eta > 0 required");
+        if (params.kmax <= 0) params.kmax = 160;
+        if (params.kmax > 1000) throw ApiError(HM_ERR_ARG, "kmax <= 1000 required");
+        check_theta(theta);
+        DeviceGuard dg(device);
+        h = new hm_handle_s();
+        h->device = device;
+        h->prm = params;
+        if (stream) {
+            h->stream = (cudaStream_t)stream;
+        } else {
+            HM_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        }
+        HM_CUDA_TRY(cudaEventCreate(&h->ev[0]));
+        HM_CUDA_TRY(cudaEventCreate(&h->ev[1]));
+        std::vector<double> hl;
+        const double* hp = locs;
+        if (locs_on_device) {
+            hl.resize(2 * n);
+            HM_CUDA_TRY(cudaMemcpy(hl.data(), locs, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+            hp = hl.data();
+        }
+        build_tree(hp, n, params.leaf, params.eta, h->T);
+        build_plan(h->T, params.kmax, h->P);
+        vm_set_attr();
+        h->pool.alloc(sizeof(double) * (size_t)std::max<int64_t>(h->P.pool_total, 1));
+        upload(h->pts, h->T.pts, h->stream);
+        upload(h->perm, h->T.perm, h->stream);
+        h->ranks.alloc(sizeof(int) * (h->P.n_slots + 1));
+        HM_CUDA_TRY(cudaMemsetAsync(h->ranks.p, 0, sizeof(int) * (h->P.n_slots + 1), h->stream));
+        h->flags.alloc(sizeof(int) * 4);
+        h->out.alloc(sizeof(double) * 3 * h->P.zw);
+        upload(h->dgen, h->P.dgen, h->stream);
+        upload(h->aca, h->P.aca, h->stream);
+        upload_phase(h->rec, h->P.recompress, h->stream);
+        upload_phase(h->chol, h->P.chol, h->stream);
+        upload_phase(h->solve, h->P.solve, h->stream);
+        upload_phase(h->lmul, h->P.lmul, h->stream);
+        do_assemble(h, theta);
+        *out = h;
+        return HM_OK;
+    } catch (...) {
+        int rc = translate_exception();
+        if (rc == HM_ERR_RANK_CAP && h) {   // handle is usable; report the cap
+            *out = h;
+            return rc;
+        }
+        delete h;
+        return rc;
+    }
+}
+
+int hm_free(hm_handle h) {
+    delete h;
+    return HM_OK;
+}
+
+int hm_assemble(hm_handle h, hm_theta theta) {
+    try {
+        if (!h) throw ApiError(HM_ERR_ARG, "null handle");
+        DeviceGuard dg(h->device);
+        do_assemble(h, theta);
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_cholesky(hm_handle h) {
+    try {
+        if (!h) throw ApiError(HM_ERR_ARG, "null handle");
+        DeviceGuard dg(h->device);
+        do_cholesky(h);
+        h->max_rank_L = max_rank(h);
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_loglik(hm_handle h, const double* Z, int32_t z_on_device, int32_t k, double* out_host) {
+    try {
+        if (!h || !Z || !out_host) throw ApiError(HM_ERR_ARG, "null pointer");
+        if (k < 1) throw ApiError(HM_ERR_ARG, "k >= 1 required");
+        DeviceGuard dg(h->device);
+        do_loglik(h, Z, z_on_device, k, out_host);
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_loglik_batch(hm_handle h, const hm_theta* thetas, int32_t n_theta, const double* Z, int32_t z_on_device,
+                    int32_t k, double* out_host) {
+    try {
+        if (!h || !thetas || !Z || !out_host) throw ApiError(HM_ERR_ARG, "null pointer");
+        if (k < 1 || n_theta < 0) throw ApiError(HM_ERR_ARG, "k >= 1, n_theta >= 0 required");
+        DeviceGuard dg(h->device);
+        int first = HM_OK;
+        for (int i = 0; i < n_theta; ++i) {
+            double* o = out_host + (int64_t)3 * k * i;
+            try {
+                do_assemble(h, thetas[i]);
+                do_cholesky(h);
+                do_loglik(h, Z, z_on_device, k, o);
+            } catch (const ApiError& e) {
+                if (first == HM_OK) first = set_error(e.code, e.what());
+                for (int c = 0; c < k; ++c) {
+                    o[3 * c] = -std::numeric_limits<double>::infinity();
+                    o[3 * c + 1] = o[3 * c + 2] = std::numeric_limits<double>::quiet_NaN();
+                }
+            }
+        }
+        return first;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k, double* Z, int32_t z_on_device) {
+    try {
+        if (!h || !xi || !Z) throw ApiError(HM_ERR_ARG, "null pointer");
+        if (k < 1) throw ApiError(HM_ERR_ARG, "k >= 1 required");
+        if (!h->factored) throw ApiError(HM_ERR_STATE, "hm_sample: call hm_cholesky first");
+        DeviceGuard dg(h->device);
+        const int64_t n = h->T.n;
+        const int zw = h->P.zw;
+        double* zt = h->pool.as<double>() + h->P.z_off;
+        h->zio.alloc(sizeof(double) * n * zw);
+        for (int c0 = 0; c0 < k; c0 += zw) {
+            const int kc = std::min(zw, k - c0);
+            const double* src = xi + (int64_t)c0 * n;
+            if (!xi_on_device) {
+                HM_CUDA_TRY(cudaMemcpyAsync(h->zio.p, src, sizeof(double) * n * kc, cudaMemcpyHostToDevice, h->stream));
+                src = h->zio.as<double>();
+            }
+            launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+            run_phase(h, h->lmul);
+            if (z_on_device) {
+                launch_scatter(zt, h->perm.as<int64_t>(), n, kc, Z + (int64_t)c0 * n, h->stream);
+            } else {
+                launch_scatter(zt, h->perm.as<int64_t>(), n, kc, h->zio.as<double>(), h->stream);
+                HM_CUDA_TRY(cudaMemcpyAsync(Z + (int64_t)c0 * n, h->zio.p, sizeof(double) * n * kc,
+                                            cudaMemcpyDeviceToHost, h->stream));
+            }
+        }
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_matvec(hm_handle h, const double*, int32_t, int32_t, double*, int32_t) {
+    (void)h;
+    return set_error(HM_ERR_STATE, "hm_matvec: not implemented in this build");
+}
+
+int hm_stats(hm_handle h, double st[12]) {
+    try {
+        if (!h || !st) throw ApiError(HM_ERR_ARG, "null pointer");
+        const Plan& P = h->P;
+        int64_t nd = 0, nl = 0;
+        double bytesC = 0, bytesL = 0;
+        DeviceGuard dg(h->device);
+        max_rank(h);
+        for (size_t b = 0; b < P.bs.size(); ++b) {
+            const BStore& s = P.bs[b];
+            if (s.kind == ST_DENSE) {
+                ++nd;
+                bytesC += 8.0 * s.m * s.p;
+            } else if (s.kind == ST_LR) {
+                ++nl;
+                bytesC += 8.0 * (s.m + s.p) * h->h_ranks[s.rslot];
+            }
+        }
+        bytesL = bytesC;   // storage of whatever the handle currently holds (C~ or L~)
+        const double n = (double)h->T.n;
+        st[0] = n;
+        st[1] = (double)nd;
+        st[2] = (double)nl;
+        st[3] = h->max_rank_C;
+        st[4] = h->max_rank_L;
+        st[5] = bytesC;
+        st[6] = bytesL;
+        st[7] = 1.0 - bytesC / (8.0 * n * n);
+        st[8] = (double)(P.chol.vt.size() + P.chol.tt.size());
+        st[9] = P.chol.nwaves;
+        st[10] = (double)P.chol.n_launches();
+        st[11] = 0;
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_timings(hm_handle h, double ms[3]) {
+    if (!h || !ms) return set_error(HM_ERR_ARG, "null pointer");
+    for (int i = 0; i < 3; ++i) ms[i] = h->ms[i];
+    return HM_OK;
+}
+
+}  // extern "C"

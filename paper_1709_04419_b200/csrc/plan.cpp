@@ -1,0 +1,778 @@
+// Host planner for the H-Cholesky, forward solve and sampler (see plan.h).
+//
+// H-Cholesky (sec. 3.1: "L~(theta;k) is the rank-k H-matrix
+// approximation of the Cholesky factor", l.263; Table 1 row "H-Cholesky",
+// l.223), right-looking recursion over the cluster tree with LAZY updates:
+//
+//   chol(t):   chol(t0);  trsm((t1,t0), L(t0,t0));  pending(t1,t1) += (t1,t0)(t1,t0)^T;  chol(t1)
+//   trsm(B=(r,s)):  X L(s,s)^T = B  recursively over the children of s;
+//                   an admissible (low-rank) B = U V^T becomes U (L(s,s)^{-1} V)^T,
+//                   i.e. an H forward substitution on the thin factor V.
+//
+// A pending update B -= X Y^T (X = (r,s), Y = (q,s)) is pushed down the
+// block tree symbolically while X and Y are subdivided; when a factor is
+// low-rank it becomes an explicit low-rank piece (U_x (Y V_x)^T, with Y V_x
+// an H-matrix x thin product), and when the target is finally needed:
+//   * a dense leaf applies all its pieces/products in one tile-VM program,
+//     then POTRF (diagonal) or TRSM (off-diagonal);
+//   * a low-rank block gathers [own U V^T, pieces, evaluated products] and is
+//     re-truncated ONCE (QR + SVD, sigma_i > eps sigma_1) -- the "truncated
+//     low-rank updates" of the north star -- then its V is forward-solved.
+// Every task declares the device regions it reads/writes (row chunks at leaf
+// clusters); a task's wave is 1 + the latest wave it depends on, so each
+// wave is a set of independent tasks executed by one launch per task type.
+#include "plan.h"
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cstdio>
+#include <stdexcept>
+#include <utility>
+
+namespace hm {
+
+int64_t Phase::n_launches() const {
+    int64_t n = 0;
+    for (int w = 0; w < nwaves; ++w) {
+        n += (v_wave_begin[w + 1] > v_wave_begin[w]) ? 1 : 0;
+        n += (t_wave_begin[w + 1] > t_wave_begin[w]) ? 1 : 0;
+    }
+    return n;
+}
+
+namespace {
+
+struct LPiece {
+    Thin U, V;       // U rows = cluster U.cluster, V rows = cluster V.cluster
+    double alpha;
+};
+
+struct Pend {
+    std::vector<std::pair<int32_t, int32_t>> prods;  // (X, Y): B -= X Y^T
+    std::vector<LPiece> pieces;
+};
+
+struct Prog {
+    std::vector<VIns> ins;
+    std::vector<int32_t> reads, writes;
+};
+
+Dim dstat(int32_t v) { return Dim{v, -1, 0, 0}; }
+Dim ddyn(int32_t stat, int32_t slot, int32_t off) { return Dim{stat, slot, off, 0}; }
+
+struct Builder {
+    const Tree& T;
+    Plan& P;
+    int64_t bump = 0;
+    int32_t nres = 0;
+    std::vector<int32_t> lw_wave, rd_wave;
+    std::vector<Pend> pend;
+    // current phase state
+    Phase* ph = nullptr;
+    std::vector<std::pair<int32_t, VTask>> vraw;   // (wave, task)
+    std::vector<std::pair<int32_t, TTask>> traw;
+    std::vector<int64_t> ws_arena;                 // per-wave workspace usage (doubles)
+    int64_t ws_max_total = 0;
+    int64_t n_tasks = 0;
+
+    Builder(const Tree& t, Plan& p) : T(t), P(p) {}
+
+    const Cluster& C(int32_t c) const { return T.clusters[c]; }
+    const Block& B(int32_t b) const { return T.blocks[b]; }
+
+    int64_t alloc(int64_t n) {
+        int64_t o = bump;
+        bump += (n + 31) & ~int64_t(31);   // 256-byte alignment
+        return o;
+    }
+    int32_t new_res(int32_t n) {
+        int32_t b = nres;
+        nres += n;
+        lw_wave.resize(nres, -1);
+        rd_wave.resize(nres, -1);
+        return b;
+    }
+
+    // ---- dependency tracking ------------------------------------------
+    int32_t wave_of(const std::vector<int32_t>& reads, const std::vector<int32_t>& writes) {
+        int32_t w = 0;
+        for (int32_t r : reads)
+            if (lw_wave[r] >= 0) w = std::max(w, lw_wave[r] + 1);
+        for (int32_t r : writes) {
+            if (lw_wave[r] >= 0) w = std::max(w, lw_wave[r] + 1);
+            if (rd_wave[r] >= 0) w = std::max(w, rd_wave[r] + 1);
+        }
+        for (int32_t r : reads) rd_wave[r] = std::max(rd_wave[r], w);
+        for (int32_t r : writes) {
+            lw_wave[r] = w;
+            rd_wave[r] = -1;
+        }
+        return w;
+    }
+
+    void emit_vm(Prog& pg) {
+        if (pg.ins.empty()) return;
+        std::sort(pg.reads.begin(), pg.reads.end());
+        pg.reads.erase(std::unique(pg.reads.begin(), pg.reads.end()), pg.reads.end());
+        std::sort(pg.writes.begin(), pg.writes.end());
+        pg.writes.erase(std::unique(pg.writes.begin(), pg.writes.end()), pg.writes.end());
+        int32_t w = wave_of(pg.reads, pg.writes);
+        VTask t;
+        t.ins_begin = (int32_t)ph->ins.size();
+        t.ins_count = (int32_t)pg.ins.size();
+        ph->ins.insert(ph->ins.end(), pg.ins.begin(), pg.ins.end());
+        vraw.push_back({w, t});
+        ++n_tasks;
+    }
+
+    // ---- thin matrices -------------------------------------------------
+    Thin sub(const Thin& M, int32_t child) const {
+        Thin s = M;
+        s.off = M.off + (C(child).lo - C(M.cluster).lo);
+        s.res0 = M.res0 + (P.leaf_begin[child] - P.leaf_begin[M.cluster]);
+        s.cluster = child;
+        return s;
+    }
+    int32_t chunk_res(const Thin& M, int32_t leafc) const {
+        return M.res0 + (P.leaf_begin[leafc] - P.leaf_begin[M.cluster]);
+    }
+    void thin_res(const Thin& M, std::vector<int32_t>& out) const {
+        for (int32_t i = 0; i < P.leaf_count[M.cluster]; ++i) out.push_back(M.res0 + i);
+    }
+    Thin new_thin(int32_t cluster, int32_t cols, int32_t slot) {
+        Thin t;
+        t.cluster = cluster;
+        t.ld = (int32_t)C(cluster).size();
+        t.cols = cols;
+        t.slot = slot;
+        t.off = alloc((int64_t)t.ld * cols);
+        t.res0 = new_res(P.leaf_count[cluster]);
+        return t;
+    }
+    Thin thin_U(int32_t b) const {
+        const BStore& s = P.bs[b];
+        Thin t;
+        t.off = s.u_off; t.ld = s.m; t.cluster = B(b).t; t.cols = s.cap; t.slot = s.rslot; t.res0 = s.u_res0;
+        return t;
+    }
+    Thin thin_V(int32_t b) const {
+        const BStore& s = P.bs[b];
+        Thin t;
+        t.off = s.v_off; t.ld = s.p; t.cluster = B(b).s; t.cols = s.cap; t.slot = s.rslot; t.res0 = s.v_res0;
+        return t;
+    }
+    // dense leaf-level block viewed as a thin matrix over its row cluster
+    Thin thin_D(int32_t b) const {
+        const BStore& s = P.bs[b];
+        Thin t;
+        t.off = s.d_off; t.ld = s.m; t.cluster = B(b).t; t.cols = s.p; t.slot = -1; t.res0 = s.d_res;
+        return t;
+    }
+
+    // VM instruction helpers
+    static VIns mk(uint8_t op) {
+        VIns i{};
+        i.op = op;
+        i.rows = dstat(0);
+        i.cols = dstat(0);
+        i.alpha = 1.0;
+        i.beta = 0.0;
+        return i;
+    }
+    // load the leaf-row chunk `leafc` of M, columns [c0, c0+64)
+    void ld_thin(Prog& pg, uint8_t tile, const Thin& M, int32_t leafc, int32_t c0) {
+        VIns i = mk(VM_LD);
+        i.t0 = tile;
+        i.rows = dstat((int32_t)C(leafc).size());
+        i.cols = (M.slot >= 0) ? ddyn(std::min(64, M.cols - c0), M.slot, c0) : dstat(std::min(64, M.cols - c0));
+        i.goff = M.off + (C(leafc).lo - C(M.cluster).lo) + (int64_t)c0 * M.ld;
+        i.ld = M.ld;
+        pg.ins.push_back(i);
+        pg.reads.push_back(chunk_res(M, leafc));
+    }
+    void st_thin(Prog& pg, uint8_t tile, const Thin& M, int32_t leafc, int32_t c0) {
+        VIns i = mk(VM_ST);
+        i.t0 = tile;
+        i.rows = dstat((int32_t)C(leafc).size());
+        i.cols = (M.slot >= 0) ? ddyn(std::min(64, M.cols - c0), M.slot, c0) : dstat(std::min(64, M.cols - c0));
+        i.goff = M.off + (C(leafc).lo - C(M.cluster).lo) + (int64_t)c0 * M.ld;
+        i.ld = M.ld;
+        pg.ins.push_back(i);
+        pg.writes.push_back(chunk_res(M, leafc));
+    }
+    void ld_dense(Prog& pg, uint8_t tile, int32_t b) {
+        const BStore& s = P.bs[b];
+        VIns i = mk(VM_LD);
+        i.t0 = tile;
+        i.rows = dstat(s.m);
+        i.cols = dstat(s.p);
+        i.goff = s.d_off;
+        i.ld = s.m;
+        pg.ins.push_back(i);
+        pg.reads.push_back(s.d_res);
+    }
+    void st_dense(Prog& pg, uint8_t tile, int32_t b) {
+        const BStore& s = P.bs[b];
+        VIns i = mk(VM_ST);
+        i.t0 = tile;
+        i.rows = dstat(s.m);
+        i.cols = dstat(s.p);
+        i.goff = s.d_off;
+        i.ld = s.m;
+        pg.ins.push_back(i);
+        pg.writes.push_back(s.d_res);
+    }
+    // small matrix (rank x width) chunk load/store; rows/cols dims given explicitly
+    void ld_small(Prog& pg, uint8_t tile, int64_t off, int32_t ld, Dim rows, Dim cols, int32_t res) {
+        VIns i = mk(VM_LD);
+        i.t0 = tile; i.rows = rows; i.cols = cols; i.goff = off; i.ld = ld;
+        pg.ins.push_back(i);
+        pg.reads.push_back(res);
+    }
+    void st_small(Prog& pg, uint8_t tile, int64_t off, int32_t ld, Dim rows, Dim cols, int32_t res) {
+        VIns i = mk(VM_ST);
+        i.t0 = tile; i.rows = rows; i.cols = cols; i.goff = off; i.ld = ld;
+        pg.ins.push_back(i);
+        pg.writes.push_back(res);
+    }
+    void zero(Prog& pg, uint8_t tile, Dim rows, Dim cols) {
+        VIns i = mk(VM_ZERO);
+        i.t0 = tile; i.rows = rows; i.cols = cols;
+        pg.ins.push_back(i);
+    }
+    void gemm(Prog& pg, uint8_t c, uint8_t a, bool ta, uint8_t b, bool tb, double alpha, double beta) {
+        VIns i = mk(VM_GEMM);
+        i.t0 = c; i.t1 = a; i.t2 = b; i.ta = ta; i.tb = tb; i.alpha = alpha; i.beta = beta;
+        pg.ins.push_back(i);
+    }
+    void op2(Prog& pg, uint8_t op, uint8_t t0, uint8_t t1, int64_t goff = 0) {
+        VIns i = mk(op);
+        i.t0 = t0; i.t1 = t1; i.goff = goff;
+        pg.ins.push_back(i);
+    }
+    Dim wdim(const Thin& M, int32_t c0) const {
+        return (M.slot >= 0) ? ddyn(std::min(64, M.cols - c0), M.slot, c0) : dstat(std::min(64, M.cols - c0));
+    }
+
+    // leaf clusters under c (in order)
+    void leaves_of(int32_t c, std::vector<int32_t>& out) const {
+        for (int32_t i = 0; i < P.leaf_count[c]; ++i) out.push_back(P.leaf_cluster[P.leaf_begin[c] + i]);
+    }
+
+    // ---- H-matrix x thin:  Tout (+)= alpha * Y * Vsrc -------------------
+    // Y: lower off-diagonal block (q, s) of any kind; Vsrc rows = s, Tout rows = q.
+    void hxt(int32_t Y, const Thin& Vsrc, const Thin& Tout, double alpha, bool accumulate) {
+        const int32_t W = Vsrc.cols;
+        // stage A: cores of the low-rank leaves, core_b = V_b^T Vsrc|_{s_b}
+        std::vector<int32_t> stack{Y}, lr_leaves;
+        const int32_t noc = (W + 63) / 64;
+        struct Core { int64_t off; int32_t res; };   // res: one resource per (kc, oc) chunk
+        std::vector<std::pair<int32_t, Core>> cores;
+        while (!stack.empty()) {
+            int32_t b = stack.back();
+            stack.pop_back();
+            const BStore& s = P.bs[b];
+            if (s.kind == ST_SUB) {
+                for (int i = 0; i < 4; ++i)
+                    if (B(b).child[i] >= 0) stack.push_back(B(b).child[i]);
+            } else if (s.kind == ST_LR) {
+                lr_leaves.push_back(b);
+            }
+        }
+        for (int32_t b : lr_leaves) {
+            const BStore& s = P.bs[b];
+            Core cr;
+            cr.off = alloc((int64_t)s.cap * W);
+            cr.res = new_res(((s.cap + 63) / 64) * noc);
+            const Thin Vb = thin_V(b);
+            const Thin Vs = sub(Vsrc, B(b).s);
+            std::vector<int32_t> lv;
+            leaves_of(B(b).s, lv);
+            for (int32_t kc = 0; kc < s.cap; kc += 64) {
+                for (int32_t oc = 0; oc < W; oc += 64) {
+                    Prog pg;
+                    Dim rows = ddyn(std::min(64, s.cap - kc), s.rslot, kc);
+                    Dim cols = wdim(Vsrc, oc);
+                    zero(pg, 0, rows, cols);
+                    for (int32_t c : lv) {
+                        ld_thin(pg, 1, Vb, c, kc);
+                        ld_thin(pg, 2, Vs, c, oc);
+                        gemm(pg, 0, 1, true, 2, false, 1.0, 1.0);
+                    }
+                    st_small(pg, 0, cr.off + kc + (int64_t)oc * s.cap, s.cap, rows, cols,
+                             cr.res + (kc / 64) * noc + oc / 64);
+                    emit_vm(pg);
+                }
+            }
+            cores.push_back({b, cr});
+        }
+        auto core_of = [&](int32_t b) -> Core {
+            for (auto& pr : cores)
+                if (pr.first == b) return pr.second;
+            throw std::logic_error("core not found");
+        };
+        // stage B: row recursion over Y carrying the active low-rank ancestors
+        struct Frame { int32_t r; std::vector<int32_t> blocks; std::vector<int32_t> active; };
+        std::vector<Frame> fs;
+        fs.push_back(Frame{B(Y).t, {Y}, {}});
+        while (!fs.empty()) {
+            Frame f = std::move(fs.back());
+            fs.pop_back();
+            std::vector<int32_t> sub_blocks, dense_here;
+            std::vector<int32_t> active = f.active;
+            for (int32_t b : f.blocks) {
+                const BStore& s = P.bs[b];
+                if (s.kind == ST_LR) active.push_back(b);
+                else if (s.kind == ST_DENSE) dense_here.push_back(b);
+                else sub_blocks.push_back(b);
+            }
+            const Cluster& rc = C(f.r);
+            if (rc.leaf()) {
+                for (int32_t oc = 0; oc < W; oc += 64) {
+                    Prog pg;
+                    if (accumulate) ld_thin(pg, 0, Tout, f.r, oc);
+                    else zero(pg, 0, dstat((int32_t)rc.size()), wdim(Tout, oc));
+                    for (int32_t b : dense_here) {
+                        ld_dense(pg, 1, b);
+                        ld_thin(pg, 2, sub(Vsrc, B(b).s), B(b).s, oc);
+                        gemm(pg, 0, 1, false, 2, false, alpha, 1.0);
+                    }
+                    for (int32_t b : active) {
+                        const BStore& s = P.bs[b];
+                        Core cr = core_of(b);
+                        const Thin Ub = thin_U(b);
+                        for (int32_t kc = 0; kc < s.cap; kc += 64) {
+                            ld_thin(pg, 1, Ub, f.r, kc);
+                            ld_small(pg, 2, cr.off + kc + (int64_t)oc * s.cap, s.cap,
+                                     ddyn(std::min(64, s.cap - kc), s.rslot, kc), wdim(Vsrc, oc),
+                                     cr.res + (kc / 64) * noc + oc / 64);
+                            gemm(pg, 0, 1, false, 2, false, alpha, 1.0);
+                        }
+                    }
+                    st_thin(pg, 0, Tout, f.r, oc);
+                    emit_vm(pg);
+                }
+                if (!sub_blocks.empty()) throw std::logic_error("hxt: subdivided block at a leaf row");
+            } else {
+                for (int i = 0; i < 2; ++i) {
+                    Frame nf;
+                    nf.r = rc.child[i];
+                    nf.active = active;
+                    for (int32_t b : sub_blocks) {
+                        // off-diagonal block children: (r_i, s_j) = child[i + 2j]
+                        for (int j = 0; j < 2; ++j) nf.blocks.push_back(B(b).child[i + 2 * j]);
+                    }
+                    fs.push_back(std::move(nf));
+                }
+            }
+        }
+    }
+
+    // ---- forward substitution  V <- L(s,s)^{-1} V --------------------------
+    void fsolve(int32_t s, const Thin& V) {
+        const int32_t d = P.diag_of[s];
+        if (C(s).leaf()) {
+            for (int32_t oc = 0; oc < V.cols; oc += 64) {
+                Prog pg;
+                ld_thin(pg, 0, V, s, oc);
+                ld_dense(pg, 1, d);
+                op2(pg, VM_TRSM_LN, 0, 1);
+                st_thin(pg, 0, V, s, oc);
+                emit_vm(pg);
+            }
+            return;
+        }
+        const int32_t s0 = C(s).child[0], s1 = C(s).child[1];
+        fsolve(s0, sub(V, s0));
+        hxt(B(d).child[1], sub(V, s0), sub(V, s1), -1.0, true);
+        fsolve(s1, sub(V, s1));
+    }
+
+    // ---- X <- L(t,t) X (sampler) -----------------------------------------
+    void lmul(int32_t t, const Thin& X) {
+        const int32_t d = P.diag_of[t];
+        if (C(t).leaf()) {
+            for (int32_t oc = 0; oc < X.cols; oc += 64) {
+                Prog pg;
+                ld_thin(pg, 0, X, t, oc);
+                ld_dense(pg, 1, d);
+                op2(pg, VM_TRMM_LN, 0, 1);
+                st_thin(pg, 0, X, t, oc);
+                emit_vm(pg);
+            }
+            return;
+        }
+        const int32_t t0 = C(t).child[0], t1 = C(t).child[1];
+        lmul(t1, sub(X, t1));
+        hxt(B(d).child[1], sub(X, t0), sub(X, t1), 1.0, true);
+        lmul(t0, sub(X, t0));
+    }
+
+    // ---- pending updates ---------------------------------------------------
+    // children of block b as (child id, i, k) with i/k the child index of its row/col cluster
+    void children(int32_t b, std::vector<std::array<int32_t, 3>>& out) const {
+        const Block& bb = B(b);
+        if (bb.t == bb.s) {
+            out.push_back({bb.child[0], 0, 0});
+            out.push_back({bb.child[1], 1, 0});
+            out.push_back({bb.child[2], 1, 1});
+        } else {
+            for (int k = 0; k < 2; ++k)
+                for (int i = 0; i < 2; ++i) out.push_back({bb.child[i + 2 * k], i, k});
+        }
+    }
+
+    void push_down(int32_t b) {
+        Pend pd = std::move(pend[b]);
+        pend[b] = Pend();
+        if (pd.prods.empty() && pd.pieces.empty()) return;
+        std::vector<std::array<int32_t, 3>> ch;
+        children(b, ch);
+        const Block& bb = B(b);
+        for (auto& pr : pd.prods) {
+            const int32_t X = pr.first, Y = pr.second;
+            const int32_t kx = P.bs[X].kind, ky = P.bs[Y].kind;
+            if (kx == ST_SUB && ky == ST_SUB) {
+                for (auto& c : ch)
+                    for (int j = 0; j < 2; ++j)
+                        pend[c[0]].prods.push_back({B(X).child[c[1] + 2 * j], B(Y).child[c[2] + 2 * j]});
+            } else if (kx == ST_LR) {
+                Thin Tm = new_thin(bb.s, P.bs[X].cap, P.bs[X].rslot);
+                hxt(Y, thin_V(X), Tm, 1.0, false);
+                pd.pieces.push_back(LPiece{thin_U(X), Tm, -1.0});
+            } else if (ky == ST_LR) {
+                Thin Tm = new_thin(bb.t, P.bs[Y].cap, P.bs[Y].rslot);
+                hxt(X, thin_V(Y), Tm, 1.0, false);
+                pd.pieces.push_back(LPiece{Tm, thin_U(Y), -1.0});
+            } else {
+                throw std::logic_error("push_down: dense factor above the leaf level");
+            }
+        }
+        for (auto& pc : pd.pieces) {
+            for (auto& c : ch) {
+                const Block& cb = B(c[0]);
+                pend[c[0]].pieces.push_back(LPiece{sub(pc.U, cb.t), sub(pc.V, cb.s), pc.alpha});
+            }
+        }
+    }
+
+    // dense leaf target: t0 holds B; apply pending products and pieces
+    void apply_dense_pending(Prog& pg, int32_t b) {
+        Pend pd = std::move(pend[b]);
+        pend[b] = Pend();
+        for (auto& pr : pd.prods) {
+            const int32_t X = pr.first, Y = pr.second;
+            if (P.bs[X].kind != ST_DENSE || P.bs[Y].kind != ST_DENSE)
+                throw std::logic_error("leaf product with non-dense factor");
+            ld_dense(pg, 1, X);
+            ld_dense(pg, 2, Y);
+            gemm(pg, 0, 1, false, 2, true, -1.0, 1.0);
+        }
+        for (auto& pc : pd.pieces) {
+            for (int32_t kc = 0; kc < pc.U.cols; kc += 64) {
+                ld_thin(pg, 1, pc.U, pc.U.cluster, kc);
+                ld_thin(pg, 2, pc.V, pc.V.cluster, kc);
+                gemm(pg, 0, 1, false, 2, true, pc.alpha, 1.0);
+            }
+        }
+    }
+
+    // evaluate product X Y^T into truncation pieces placed at (row0, col0) of the target
+    void eval_pieces(int32_t X, int32_t Y, int32_t row0, int32_t col0, std::vector<TPiece>& out,
+                     std::vector<int32_t>& reads) {
+        const int32_t kx = P.bs[X].kind, ky = P.bs[Y].kind;
+        if (kx == ST_LR) {
+            Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot);
+            hxt(Y, thin_V(X), Tm, 1.0, false);
+            out.push_back(tpiece(thin_U(X), Tm, row0, col0, -1.0, reads));
+        } else if (ky == ST_LR) {
+            Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot);
+            hxt(X, thin_V(Y), Tm, 1.0, false);
+            out.push_back(tpiece(Tm, thin_U(Y), row0, col0, -1.0, reads));
+        } else if (kx == ST_DENSE && ky == ST_DENSE) {
+            out.push_back(tpiece(thin_D(X), thin_D(Y), row0, col0, -1.0, reads));
+        } else if (kx == ST_SUB && ky == ST_SUB) {
+            const Cluster& rx = C(B(X).t);
+            const Cluster& ry = C(B(Y).t);
+            for (int i = 0; i < 2; ++i)
+                for (int k = 0; k < 2; ++k)
+                    for (int j = 0; j < 2; ++j) {
+                        const int32_t cx = B(X).child[i + 2 * j], cy = B(Y).child[k + 2 * j];
+                        eval_pieces(cx, cy, row0 + (int32_t)(C(B(cx).t).lo - rx.lo),
+                                    col0 + (int32_t)(C(B(cy).t).lo - ry.lo), out, reads);
+                    }
+        } else {
+            throw std::logic_error("eval_pieces: mixed dense/subdivided factors");
+        }
+    }
+
+    TPiece tpiece(const Thin& U, const Thin& V, int32_t row0, int32_t col0, double alpha,
+                  std::vector<int32_t>& reads) {
+        TPiece p{};
+        p.u_off = U.off; p.u_ld = U.ld; p.u_row0 = row0; p.u_rows = (int32_t)C(U.cluster).size();
+        p.v_off = V.off; p.v_ld = V.ld; p.v_row0 = col0; p.v_rows = (int32_t)C(V.cluster).size();
+        p.w = (U.slot >= 0) ? ddyn(U.cols, U.slot, 0) : dstat(U.cols);
+        p.alpha = alpha;
+        thin_res(U, reads);
+        thin_res(V, reads);
+        return p;
+    }
+
+    // low-rank target: gather own + pending and re-truncate once
+    void flush_lr(int32_t b, bool force) {
+        Pend pd = std::move(pend[b]);
+        pend[b] = Pend();
+        if (!force && pd.prods.empty() && pd.pieces.empty()) return;
+        const BStore& s = P.bs[b];
+        std::vector<TPiece> pcs;
+        std::vector<int32_t> reads, writes;
+        pcs.push_back(tpiece(thin_U(b), thin_V(b), 0, 0, 1.0, reads));
+        for (auto& pc : pd.pieces) pcs.push_back(tpiece(pc.U, pc.V, 0, 0, pc.alpha, reads));
+        for (auto& pr : pd.prods) eval_pieces(pr.first, pr.second, 0, 0, pcs, reads);
+        thin_res(thin_U(b), writes);
+        thin_res(thin_V(b), writes);
+        emit_trunc(b, pcs, reads, writes);
+    }
+
+    void emit_trunc(int32_t b, const std::vector<TPiece>& pcs, std::vector<int32_t>& reads,
+                    std::vector<int32_t>& writes) {
+        const BStore& s = P.bs[b];
+        std::sort(reads.begin(), reads.end());
+        reads.erase(std::unique(reads.begin(), reads.end()), reads.end());
+        int32_t w = wave_of(reads, writes);
+        TTask t{};
+        t.u_out = s.u_off; t.v_out = s.v_off;
+        t.m = s.m; t.q = s.p; t.cap = s.cap; t.rslot = s.rslot;
+        t.piece_begin = (int32_t)ph->tp.size();
+        t.piece_count = (int32_t)pcs.size();
+        int32_t kt = 0;
+        for (auto& p : pcs) kt += p.w.stat;
+        t.kmax_tot = kt;
+        const int64_t K = kt;
+        t.ws_size = ((int64_t)s.m + s.p + 2 * K + 8) * K + 64;
+        if ((int)ws_arena.size() <= w) ws_arena.resize(w + 1, 0);
+        t.ws = ws_arena[w];           // relative; rebased after planning
+        ws_arena[w] += (t.ws_size + 31) & ~int64_t(31);
+        ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
+        traw.push_back({w, t});
+        ++n_tasks;
+    }
+
+    // ---- H-Cholesky recursion -----------------------------------------------
+    void chol(int32_t t) {
+        const int32_t d = P.diag_of[t];
+        if (P.bs[d].kind == ST_SUB) {
+            push_down(d);
+            const int32_t t0 = C(t).child[0], t1 = C(t).child[1];
+            chol(t0);
+            const int32_t off = B(d).child[1];   // (t1, t0)
+            trsm(off);
+            pend[B(d).child[2]].prods.push_back({off, off});
+            chol(t1);
+        } else {
+            Prog pg;
+            ld_dense(pg, 0, d);
+            apply_dense_pending(pg, d);
+            const int32_t li = P.leaf_begin[t];
+            op2(pg, VM_POTRF, 0, 0, P.logd_off + li);
+            st_dense(pg, 0, d);
+            emit_vm(pg);
+        }
+    }
+
+    void trsm(int32_t b) {
+        const Block& bb = B(b);
+        const int32_t s = bb.s;
+        const BStore& st = P.bs[b];
+        if (st.kind == ST_SUB) {
+            push_down(b);
+            const int32_t ds = P.diag_of[s];
+            for (int i = 0; i < 2; ++i) trsm(bb.child[i]);                     // (r_i, s0)
+            for (int i = 0; i < 2; ++i) pend[bb.child[i + 2]].prods.push_back({bb.child[i], B(ds).child[1]});
+            for (int i = 0; i < 2; ++i) trsm(bb.child[i + 2]);                 // (r_i, s1)
+        } else if (st.kind == ST_DENSE) {
+            Prog pg;
+            ld_dense(pg, 0, b);
+            apply_dense_pending(pg, b);
+            ld_dense(pg, 3, P.diag_of[s]);
+            op2(pg, VM_TRSM_RLT, 0, 3);
+            st_dense(pg, 0, b);
+            emit_vm(pg);
+        } else {
+            flush_lr(b, false);
+            fsolve(s, thin_V(b));
+        }
+    }
+
+    // ---- phase bookkeeping -------------------------------------------------
+    void begin_phase(Phase& p) {
+        ph = &p;
+        vraw.clear();
+        traw.clear();
+        ws_arena.clear();
+        std::fill(lw_wave.begin(), lw_wave.end(), -1);
+        std::fill(rd_wave.begin(), rd_wave.end(), -1);
+    }
+    void end_phase() {
+        int32_t nw = 0;
+        for (auto& v : vraw) nw = std::max(nw, v.first + 1);
+        for (auto& v : traw) nw = std::max(nw, v.first + 1);
+        std::stable_sort(vraw.begin(), vraw.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        std::stable_sort(traw.begin(), traw.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        ph->nwaves = nw;
+        ph->v_wave_begin.assign(nw + 1, 0);
+        ph->t_wave_begin.assign(nw + 1, 0);
+        ph->vt.clear();
+        ph->tt.clear();
+        {
+            size_t k = 0;
+            for (int32_t w = 0; w < nw; ++w) {
+                ph->v_wave_begin[w] = (int32_t)k;
+                while (k < vraw.size() && vraw[k].first == w) ph->vt.push_back(vraw[k++].second);
+            }
+            ph->v_wave_begin[nw] = (int32_t)k;
+        }
+        // workspace: arenas are reused across waves (tasks of one wave run concurrently)
+        int64_t ws_need = 0;
+        for (auto x : ws_arena) ws_need = std::max(ws_need, x);
+        const int64_t ws_base = alloc(ws_need);
+        {
+            size_t k = 0;
+            for (int32_t w = 0; w < nw; ++w) {
+                ph->t_wave_begin[w] = (int32_t)k;
+                while (k < traw.size() && traw[k].first == w) {
+                    TTask t = traw[k++].second;
+                    t.ws += ws_base;
+                    ph->tt.push_back(t);
+                }
+            }
+            ph->t_wave_begin[nw] = (int32_t)k;
+        }
+        ph = nullptr;
+    }
+};
+
+}  // namespace
+
+std::string Plan::summary() const {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf),
+                  "blocks=%zu leaves=%d slots=%d pool_blocks=%.3f GB pool_total=%.3f GB | chol: %zu vm + %zu trunc "
+                  "tasks, %d waves, %lld launches | solve: %zu tasks, %d waves",
+                  bs.size(), n_leaves, n_slots, pool_blocks * 8e-9, pool_total * 8e-9, chol.vt.size(), chol.tt.size(),
+                  chol.nwaves, (long long)chol.n_launches(), solve.vt.size() + solve.tt.size(), solve.nwaves);
+    return buf;
+}
+
+void build_plan(const Tree& T, int32_t kmax, Plan& P) {
+    if (T.leaf > 64) throw std::invalid_argument("leaf size > 64 is not supported by the tile VM");
+    P = Plan();
+    P.kmax = kmax;
+    const int32_t nc = (int32_t)T.clusters.size();
+    // leaves in tree order and per-cluster leaf ranges
+    P.leaf_begin.assign(nc, 0);
+    P.leaf_count.assign(nc, 0);
+    int32_t leaf_depth = -1;
+    {
+        std::vector<int32_t> order;   // pre-order == storage order; leaves appear in index order
+        for (int32_t c = 0; c < nc; ++c)
+            if (T.clusters[c].leaf()) {
+                P.leaf_cluster.push_back(c);
+                if (leaf_depth < 0) leaf_depth = T.clusters[c].level;
+                else if (leaf_depth != T.clusters[c].level)
+                    throw std::invalid_argument(
+                        "unsupported geometry: leaf clusters at different depths (n / 2^l straddles the leaf size)");
+            }
+        P.n_leaves = (int32_t)P.leaf_cluster.size();
+        // leaf_begin via post-order accumulation (children after parents in pre-order: iterate backwards)
+        std::vector<int32_t> first(nc, INT32_MAX);
+        for (int32_t i = 0; i < P.n_leaves; ++i) {
+            first[P.leaf_cluster[i]] = i;
+            P.leaf_count[P.leaf_cluster[i]] = 1;
+        }
+        for (int32_t c = nc - 1; c >= 0; --c) {
+            const Cluster& cl = T.clusters[c];
+            if (!cl.leaf()) {
+                first[c] = std::min(first[cl.child[0]], first[cl.child[1]]);
+                P.leaf_count[c] = P.leaf_count[cl.child[0]] + P.leaf_count[cl.child[1]];
+            }
+        }
+        for (int32_t c = 0; c < nc; ++c) P.leaf_begin[c] = first[c];
+    }
+    Builder bld(T, P);
+    // block storage
+    const int32_t nb = (int32_t)T.blocks.size();
+    P.bs.assign(nb, BStore());
+    P.diag_of.assign(nc, -1);
+    for (int32_t b = 0; b < nb; ++b) {
+        const Block& bk = T.blocks[b];
+        if (bk.t == bk.s) P.diag_of[bk.t] = b;
+        BStore& s = P.bs[b];
+        const Cluster& ct = T.clusters[bk.t];
+        const Cluster& cs = T.clusters[bk.s];
+        s.m = (int32_t)ct.size();
+        s.p = (int32_t)cs.size();
+        const bool leafpair = ct.leaf() && cs.leaf();
+        if (bk.kind == BK_SUB) {
+            s.kind = ST_SUB;
+        } else if (bk.kind == BK_DENSE || leafpair) {
+            s.kind = ST_DENSE;
+            s.d_off = bld.alloc((int64_t)s.m * s.p);
+            s.d_res = bld.new_res(1);
+            P.bytes_C += 8LL * s.m * s.p;
+        } else {
+            s.kind = ST_LR;
+            s.cap = std::min(kmax, std::min(s.m, s.p));
+            s.rslot = P.n_slots++;
+            s.u_off = bld.alloc((int64_t)s.m * s.cap);
+            s.v_off = bld.alloc((int64_t)s.p * s.cap);
+            s.u_res0 = bld.new_res(P.leaf_count[bk.t]);
+            s.v_res0 = bld.new_res(P.leaf_count[bk.s]);
+            P.bytes_C += 8LL * (s.m + s.p) * s.cap;
+        }
+    }
+    P.logd_off = bld.alloc(P.n_leaves);
+    P.zw = 64;
+    P.z_off = bld.alloc((int64_t)T.n * P.zw);
+    const int32_t z_res0 = bld.new_res(P.n_leaves);
+    P.pool_blocks = bld.bump;
+    // assembly tasks
+    for (int32_t b = 0; b < nb; ++b) {
+        const Block& bk = T.blocks[b];
+        const BStore& s = P.bs[b];
+        const Cluster& ct = T.clusters[bk.t];
+        const Cluster& cs = T.clusters[bk.s];
+        if (s.kind == ST_DENSE) {
+            P.dgen.push_back(DenseGenTask{s.d_off, (int32_t)ct.lo, (int32_t)cs.lo, s.m, s.p});
+        } else if (s.kind == ST_LR) {
+            P.aca.push_back(AcaTask{s.u_off, s.v_off, (int32_t)ct.lo, (int32_t)cs.lo, s.m, s.p, s.cap, s.rslot});
+        }
+    }
+    bld.pend.assign(nb, Pend());
+    // recompression of every ACA block: a truncation with the block itself as the only piece
+    bld.begin_phase(P.recompress);
+    for (int32_t b = 0; b < nb; ++b)
+        if (P.bs[b].kind == ST_LR) bld.flush_lr(b, true);
+    bld.end_phase();
+    // H-Cholesky
+    bld.begin_phase(P.chol);
+    bld.n_tasks = 0;
+    bld.chol(0);
+    P.n_tasks_chol = bld.n_tasks;
+    bld.end_phase();
+    for (auto& pd : bld.pend)
+        if (!pd.prods.empty() || !pd.pieces.empty()) throw std::logic_error("planner: unapplied pending update");
+    // forward solve and sampler on the z buffer (rows = root cluster, tree order)
+    Thin Z;
+    Z.off = P.z_off; Z.ld = (int32_t)T.n; Z.cluster = 0; Z.cols = P.zw; Z.slot = -1; Z.res0 = z_res0;
+    bld.begin_phase(P.solve);
+    bld.fsolve(0, Z);
+    bld.end_phase();
+    bld.begin_phase(P.lmul);
+    bld.lmul(0, Z);
+    bld.end_phase();
+    P.pool_total = bld.bump;
+}
+
+}  // namespace hm

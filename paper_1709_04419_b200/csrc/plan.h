@@ -1,0 +1,84 @@
+// Host planner: symbolic H-Cholesky / forward-solve / sampler (PAPER.md
+// sec. 3.1-3.2, l.259-283) lowered to a DAG of device tasks, levelled into
+// waves.  The plan depends only on the geometry (tree, partition, leaf, eta,
+// kmax) -- never on theta -- so it is built once per location set and replayed
+// for every likelihood evaluation; ranks are read by the kernels at run time
+// from rank slots in device memory.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hm_tasks.h"
+#include "tree.h"
+
+namespace hm {
+
+// storage of one lower block of the partition
+enum StoreKind : int32_t { ST_SUB = 0, ST_DENSE = 1, ST_LR = 2 };
+
+struct BStore {
+    int32_t kind = ST_SUB;
+    int32_t m = 0, p = 0;        // rows |t|, cols |s|
+    int64_t d_off = -1;          // dense m x p (ld m)
+    int64_t u_off = -1, v_off = -1;
+    int32_t cap = 0, rslot = -1;
+    int32_t d_res = -1;          // resource id (dense)
+    int32_t u_res0 = -1, v_res0 = -1;  // first leaf-chunk resource of U (rows t) / V (rows s)
+};
+
+// A matrix whose rows are the points of a cluster (tree order), split into
+// row chunks at that cluster's leaf clusters for dependency tracking.
+struct Thin {
+    int64_t off = -1;
+    int32_t ld = 0;
+    int32_t cluster = -1;
+    int32_t cols = 0;            // static (maximum) number of columns
+    int32_t slot = -1;           // rank slot giving the actual column count (-1: static)
+    int32_t res0 = -1;           // resource id of the chunk of the first leaf of `cluster`
+};
+
+struct Phase {                   // one executable phase (levelled task lists)
+    std::vector<VIns> ins;
+    std::vector<VTask> vt;       // sorted by wave
+    std::vector<TTask> tt;       // sorted by wave
+    std::vector<TPiece> tp;
+    std::vector<int32_t> v_wave_begin, t_wave_begin;  // size nwaves + 1
+    int32_t nwaves = 0;
+    int64_t n_launches() const;
+};
+
+struct Plan {
+    // geometry-derived layout
+    std::vector<BStore> bs;
+    std::vector<int32_t> diag_of;      // cluster -> diagonal block id
+    std::vector<int32_t> leaf_begin;   // cluster -> index of its first leaf cluster
+    std::vector<int32_t> leaf_count;
+    std::vector<int32_t> leaf_cluster; // leaf index -> cluster id
+    std::vector<int32_t> leaf_diag_idx;// leaf index -> logd index (== leaf index)
+    int32_t n_leaves = 0;
+    int32_t n_slots = 0;
+    int32_t kmax = 0;
+    int64_t pool_blocks = 0;           // doubles used by block storage (C~ / L~)
+    int64_t pool_total = 0;            // doubles incl. temporaries and workspaces
+    int64_t logd_off = 0;              // n_leaves doubles
+    int64_t z_off = 0;                 // solve RHS buffer: n x ZW (col-major, ld n)
+    int32_t zw = 64;
+    int64_t bytes_C = 0;               // bytes of block storage at capacity
+    // assembly
+    std::vector<DenseGenTask> dgen;
+    std::vector<AcaTask> aca;
+    Phase recompress;                  // TRUNC of every LR block after ACA
+    // factorisation and solves
+    Phase chol;
+    Phase solve;                       // v <- L~^{-1} z  on the z buffer
+    Phase lmul;                        // z <- L~ z       (sampler)
+    int64_t n_tasks_chol = 0;
+    std::string summary() const;
+};
+
+// Build the full plan for a tree.  Throws std::invalid_argument for
+// unsupported geometry (leaf > 64, leaves at different depths).
+void build_plan(const Tree& T, int32_t kmax, Plan& P);
+
+}  // namespace hm

@@ -1,0 +1,234 @@
+"""Test-only CPU interpreter of the H-Cholesky task DAG (host planner output).
+
+It executes the tasks that ``hm_plan_dump`` writes -- the exact programs the
+GPU tile VM and truncation kernel run -- with numpy, visiting the tasks of
+each wave in a RANDOM order.  Comparing its log-likelihood with the dense
+oracle therefore checks the planner's H-arithmetic (update bookkeeping,
+pushes, products, truncation pieces) and its dependency analysis (a missing
+edge inside a wave shows up as an order-dependent wrong answer) without a GPU.
+
+Block entries and the initial low-rank factors come from ``oracle`` (dense
+Matern blocks + exact truncated SVD), not from the CUDA kernels: this file
+validates host logic only and is never reachable from the product path.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from oracle.matern import matern
+
+DIM = np.dtype([("stat", "<i4"), ("slot", "<i4"), ("off", "<i4"), ("pad", "<i4")])
+VINS = np.dtype([("op", "u1"), ("t0", "u1"), ("t1", "u1"), ("t2", "u1"), ("ta", "u1"), ("tb", "u1"),
+                 ("p0", "u1"), ("p1", "u1"), ("rows", DIM), ("cols", DIM), ("goff", "<i8"), ("ld", "<i4"),
+                 ("p2", "<i4"), ("alpha", "<f8"), ("beta", "<f8")])
+VTASK = np.dtype([("ins_begin", "<i4"), ("ins_count", "<i4")])
+TTASK = np.dtype([("u_out", "<i8"), ("v_out", "<i8"), ("ws", "<i8"), ("ws_size", "<i8"), ("m", "<i4"),
+                  ("q", "<i4"), ("cap", "<i4"), ("rslot", "<i4"), ("piece_begin", "<i4"), ("piece_count", "<i4"),
+                  ("kmax_tot", "<i4"), ("pad", "<i4")])
+TPIECE = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("u_ld", "<i4"), ("v_ld", "<i4"), ("u_row0", "<i4"),
+                   ("u_rows", "<i4"), ("v_row0", "<i4"), ("v_rows", "<i4"), ("w", DIM), ("alpha", "<f8")])
+DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4")])
+ACA = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4"),
+                ("cap", "<i4"), ("rslot", "<i4")])
+
+VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO = range(1, 9)
+TD = 64
+
+
+def _read(path):
+    raw = open(path, "rb").read()
+    pos = 0
+    out = []
+    while pos < len(raw):
+        cnt, size = np.frombuffer(raw, "<i8", 2, pos)
+        pos += 16
+        out.append((int(cnt), int(size), raw[pos:pos + cnt * size]))
+        pos += cnt * size
+    return out
+
+
+class Phase:
+    def __init__(self, secs):
+        (ni, si, bi), (nv, sv, bv), (nt, st, bt), (np_, sp, bp), (nw1, _, bw1), (nw2, _, bw2) = secs
+        assert si == VINS.itemsize and sv == VTASK.itemsize and st == TTASK.itemsize and sp == TPIECE.itemsize
+        self.ins = np.frombuffer(bi, VINS, ni)
+        self.vt = np.frombuffer(bv, VTASK, nv)
+        self.tt = np.frombuffer(bt, TTASK, nt)
+        self.tp = np.frombuffer(bp, TPIECE, np_)
+        self.vwb = np.frombuffer(bw1, "<i4", nw1)
+        self.twb = np.frombuffer(bw2, "<i4", nw2)
+        self.nwaves = max(len(self.vwb) - 1, 0)
+
+
+class Plan:
+    def __init__(self, path):
+        secs = _read(path)
+        hdr = np.frombuffer(secs[0][2], "<i8", 8)
+        (self.pool_total, self.n_slots, self.logd_off, self.z_off, self.zw, self.n, self.n_leaves, _) = map(int, hdr)
+        assert secs[1][1] == DGEN.itemsize and secs[2][1] == ACA.itemsize
+        self.dgen = np.frombuffer(secs[1][2], DGEN, secs[1][0])
+        self.aca = np.frombuffer(secs[2][2], ACA, secs[2][0])
+        self.phases = [Phase(secs[3 + 6 * i: 9 + 6 * i]) for i in range(4)]
+        self.recompress, self.chol, self.solve, self.lmul = self.phases
+
+
+class Interp:
+    def __init__(self, plan: Plan, eps: float, seed: int = 0):
+        self.P = plan
+        self.eps = eps
+        self.pool = np.zeros(plan.pool_total)
+        self.ranks = np.zeros(max(plan.n_slots, 1), dtype=np.int64)
+        self.rng = np.random.default_rng(seed)
+        self.fail = 0
+
+    # ---------------------------------------------------------------- helpers
+    def dim(self, d):
+        if d["slot"] < 0:
+            return int(d["stat"])
+        v = int(self.ranks[d["slot"]]) - int(d["off"])
+        return max(0, min(v, int(d["stat"])))
+
+    def gload(self, off, ld, r, c):
+        if r == 0 or c == 0:
+            return np.zeros((r, c))
+        idx = off + np.arange(r)[:, None] + ld * np.arange(c)[None, :]
+        return self.pool[idx]
+
+    def gstore(self, off, ld, M):
+        r, c = M.shape
+        if r == 0 or c == 0:
+            return
+        idx = off + np.arange(r)[:, None] + ld * np.arange(c)[None, :]
+        self.pool[idx] = M
+
+    # ---------------------------------------------------------------- assembly (oracle entries)
+    def assemble(self, pts_tree, theta):
+        s2, ell, nu = theta
+
+        def block(r0, c0, m, q):
+            a = pts_tree[r0:r0 + m]
+            b = pts_tree[c0:c0 + q]
+            h = np.sqrt(((a[:, None, :] - b[None, :, :]) ** 2).sum(-1))
+            return matern(h.ravel(), s2, ell, nu).reshape(m, q)
+
+        for t in self.P.dgen:
+            self.gstore(int(t["off"]), int(t["m"]), block(int(t["r0"]), int(t["c0"]), int(t["m"]), int(t["q"])))
+        for t in self.P.aca:
+            M = block(int(t["r0"]), int(t["c0"]), int(t["m"]), int(t["q"]))
+            U, S, Vt = np.linalg.svd(M, full_matrices=False)
+            r = int(np.sum(S > 0.25 * self.eps * S[0]))
+            r = min(r, int(t["cap"]))
+            self.gstore(int(t["u_off"]), int(t["m"]), U[:, :r] * S[:r])
+            self.gstore(int(t["v_off"]), int(t["q"]), Vt[:r].T)
+            self.ranks[t["rslot"]] = r
+        self.run(self.P.recompress)
+
+    # ---------------------------------------------------------------- tasks
+    def vm(self, ph, task):
+        tiles = [np.zeros((0, 0)) for _ in range(5)]
+        for I in ph.ins[task["ins_begin"]: task["ins_begin"] + task["ins_count"]]:
+            op = int(I["op"])
+            if op == VM_LD:
+                tiles[I["t0"]] = self.gload(int(I["goff"]), int(I["ld"]), self.dim(I["rows"]), self.dim(I["cols"]))
+            elif op == VM_ST:
+                T = tiles[I["t0"]]
+                r, c = min(self.dim(I["rows"]), T.shape[0]), min(self.dim(I["cols"]), T.shape[1])
+                self.gstore(int(I["goff"]), int(I["ld"]), T[:r, :c])
+            elif op == VM_ZERO:
+                tiles[I["t0"]] = np.zeros((self.dim(I["rows"]), self.dim(I["cols"])))
+            elif op == VM_GEMM:
+                A = tiles[I["t1"]].T if I["ta"] else tiles[I["t1"]]
+                B = tiles[I["t2"]].T if I["tb"] else tiles[I["t2"]]
+                k = max(A.shape[1], B.shape[0])
+                A2 = np.zeros((A.shape[0], k)); A2[:, :A.shape[1]] = A
+                B2 = np.zeros((k, B.shape[1])); B2[:B.shape[0], :] = B
+                prod = I["alpha"] * (A2 @ B2)
+                if I["beta"] == 0.0:
+                    tiles[I["t0"]] = prod
+                else:
+                    C = tiles[I["t0"]].copy()
+                    C[:prod.shape[0], :prod.shape[1]] = I["beta"] * C[:prod.shape[0], :prod.shape[1]] + prod
+                    tiles[I["t0"]] = C
+            elif op == VM_POTRF:
+                A = tiles[I["t0"]]
+                A = np.tril(A) + np.tril(A, -1).T
+                try:
+                    L = np.linalg.cholesky(A)
+                except np.linalg.LinAlgError:
+                    self.fail += 1
+                    L = np.eye(A.shape[0])
+                tiles[I["t0"]] = L
+                self.pool[int(I["goff"])] = float(np.sum(np.log(np.diag(L))))
+            elif op == VM_TRSM_RLT:       # B <- B L^{-T}
+                B, L = tiles[I["t0"]], tiles[I["t1"]][:tiles[I["t0"]].shape[1], :tiles[I["t0"]].shape[1]]
+                tiles[I["t0"]] = np.linalg.solve(np.tril(L), B.T).T
+            elif op == VM_TRSM_LN:        # B <- L^{-1} B
+                B = tiles[I["t0"]]
+                L = np.tril(tiles[I["t1"]][:B.shape[0], :B.shape[0]])
+                tiles[I["t0"]] = np.linalg.solve(L, B)
+            elif op == VM_TRMM_LN:
+                B = tiles[I["t0"]]
+                L = np.tril(tiles[I["t1"]][:B.shape[0], :B.shape[0]])
+                tiles[I["t0"]] = L @ B
+            else:
+                raise ValueError(op)
+
+    def trunc(self, ph, t):
+        m, q = int(t["m"]), int(t["q"])
+        As, Bs = [], []
+        for pc in ph.tp[t["piece_begin"]: t["piece_begin"] + t["piece_count"]]:
+            w = self.dim(pc["w"])
+            A = np.zeros((m, w)); B = np.zeros((q, w))
+            A[pc["u_row0"]:pc["u_row0"] + pc["u_rows"]] = pc["alpha"] * self.gload(int(pc["u_off"]), int(pc["u_ld"]),
+                                                                                  int(pc["u_rows"]), w)
+            B[pc["v_row0"]:pc["v_row0"] + pc["v_rows"]] = self.gload(int(pc["v_off"]), int(pc["v_ld"]),
+                                                                     int(pc["v_rows"]), w)
+            As.append(A); Bs.append(B)
+        A = np.concatenate(As, axis=1); B = np.concatenate(Bs, axis=1)
+        if A.shape[1] == 0:
+            self.ranks[t["rslot"]] = 0
+            return
+        Qa, Ra = np.linalg.qr(A)
+        Qb, Rb = np.linalg.qr(B)
+        W, S, Zt = np.linalg.svd(Ra @ Rb.T)
+        r = int(np.sum((S > self.eps * S[0]) & (S > 0))) if S.size else 0
+        r = min(r, int(t["cap"]))
+        self.gstore(int(t["u_out"]), m, (Qa @ W[:, :r]) * S[:r])
+        self.gstore(int(t["v_out"]), q, Qb @ Zt[:r].T)
+        self.ranks[t["rslot"]] = r
+
+    def run(self, ph):
+        for w in range(ph.nwaves):
+            jobs = [("v", i) for i in range(ph.vwb[w], ph.vwb[w + 1])] + \
+                   [("t", i) for i in range(ph.twb[w], ph.twb[w + 1])]
+            for kind, i in [jobs[j] for j in self.rng.permutation(len(jobs))]:
+                if kind == "v":
+                    self.vm(ph, ph.vt[i])
+                else:
+                    self.trunc(ph, ph.tt[i])
+
+    # ---------------------------------------------------------------- likelihood
+    def loglik(self, Z_tree):
+        n, zw = self.P.n, self.P.zw
+        Z_tree = np.asarray(Z_tree).reshape(n, -1)
+        k = Z_tree.shape[1]
+        buf = np.zeros((n, zw))
+        buf[:, :k] = Z_tree
+        self.pool[self.P.z_off:self.P.z_off + n * zw] = buf.ravel(order="F")
+        self.run(self.P.solve)
+        v = self.pool[self.P.z_off:self.P.z_off + n * zw].reshape(zw, n).T[:, :k]
+        logdet = 2.0 * float(np.sum(self.pool[self.P.logd_off:self.P.logd_off + self.P.n_leaves]))
+        quad = np.sum(v * v, axis=0)
+        return -0.5 * n * math.log(2 * math.pi) - 0.5 * logdet - 0.5 * quad, logdet, quad
+
+    def lmul(self, X_tree):
+        n, zw = self.P.n, self.P.zw
+        X_tree = np.asarray(X_tree).reshape(n, -1)
+        k = X_tree.shape[1]
+        buf = np.zeros((n, zw))
+        buf[:, :k] = X_tree
+        self.pool[self.P.z_off:self.P.z_off + n * zw] = buf.ravel(order="F")
+        self.run(self.P.lmul)
+        return self.pool[self.P.z_off:self.P.z_off + n * zw].reshape(zw, n).T[:, :k].copy()

@@ -1,0 +1,85 @@
+"""GPU parity of the device Matern kernel and the dense fp64 check path against
+the oracle (Eq. 1 and Eq. 2).  Tolerance: 1e-10 relative on the
+log-likelihood (north star), 1e-12 relative on kernel entries."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dense as odense
+from oracle.matern import matern as omatern
+from synthetic import uniform_iid, standard_normal, perturbed_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hm(gpu_required):
+    import paper_1709_04419_b200 as hm
+    return hm
+
+
+@pytest.mark.parametrize("nu", [0.5, 1.5, 2.5, 1.0, 0.35, 0.73, 3.2, 0.1, 5.6])
+def test_matern_kernel_vs_oracle(hm, nu):
+    rng = np.random.default_rng(17)
+    a = rng.random((64, 2))
+    b = rng.random((50, 2)) * 3.0
+    theta = (1.7, 0.13, nu)
+    got = hm.matern_block(a, b, theta)
+    h = np.sqrt(((a[:, None, :] - b[None, :, :]) ** 2).sum(-1))
+    want = omatern(h.ravel(), *theta).reshape(h.shape)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-300)
+    # zero lag and tiny lags (continuity)
+    z = hm.matern_block(np.array([[0.2, 0.2]]), np.array([[0.2, 0.2], [0.2, 0.2 + 1e-9]]), theta)
+    assert z[0, 0] == 1.7
+    assert z[0, 1] == pytest.approx(omatern(1e-9, *theta)[0], rel=1e-12)
+
+
+def _check_dense(hm, pts, theta, Z, rtol=1e-10):
+    got = hm.dense_loglik(pts, theta, Z)
+    ll, ld, q = odense.loglik(pts, Z, theta, bessel="quad" if len(pts) <= 2500 else "scipy")
+    ll, q = np.atleast_1d(ll), np.atleast_1d(q)
+    np.testing.assert_allclose(got[:, 0], ll, rtol=rtol)
+    np.testing.assert_allclose(got[:, 1], ld, rtol=rtol, atol=rtol * len(pts))
+    np.testing.assert_allclose(got[:, 2], q, rtol=rtol)
+
+
+def test_dense_config0(hm):
+    # configs[0]: n = 2000 uniform, sigma^2 = 1, ell = 0.0864, nu = 0.5, Z = L N(0, I)
+    pts = uniform_iid(2000, seed=0)
+    theta = (1.0, 0.0864, 0.5)
+    Z = odense.sample(pts, theta, standard_normal(2000, 1, seed=1))
+    _check_dense(hm, pts, theta, Z)
+
+
+@pytest.mark.parametrize("n,nu,k", [(777, 1.0, 1), (1, 0.5, 1), (63, 1.5, 3), (65, 0.35, 2), (1500, 2.2, 70)])
+def test_dense_ragged_general_nu(hm, n, nu, k):
+    pts = uniform_iid(n, seed=n)
+    theta = (1.3, 0.11, nu)
+    Z = standard_normal(n, k, seed=2)
+    _check_dense(hm, pts, theta, Z)
+
+
+def test_dense_16k(hm):
+    # configs[1] size, nu = 1.5 (closed-form path on the device, Bessel quadrature/scipy in the oracle)
+    pts = uniform_iid(16384, seed=1)
+    theta = (1.0, 0.2, 1.5)
+    Z = standard_normal(16384, 1, seed=3)
+    _check_dense(hm, pts, theta, Z)
+
+
+def test_dense_device_pointers(hm):
+    import torch
+    pts = uniform_iid(500, seed=5)
+    Z = standard_normal(500, 2, seed=6)
+    theta = (1.0, 0.1, 0.8)
+    host = hm.dense_loglik(pts, theta, Z)
+    dev = hm.dense_loglik(torch.tensor(pts, device="cuda"), theta, torch.tensor(Z.T.copy(), device="cuda"))
+    np.testing.assert_allclose(dev, host, rtol=1e-13)
+
+
+def test_dense_errors(hm):
+    with pytest.raises(hm.HMError):
+        hm.dense_loglik(uniform_iid(10, 0), (1.0, -0.1, 0.5), np.zeros(10))
+    with pytest.raises(hm.HMError):
+        hm.dense_loglik(uniform_iid(16385, 0), (1.0, 0.1, 0.5), np.zeros(16385))

@@ -1,0 +1,95 @@
+"""Host-logic test of the H-Cholesky planner (no GPU): the task DAG that the
+GPU executes is interpreted on the CPU (tests/plan_interp.py) with tasks of each
+wave in random order, and the resulting log-likelihood (Eq. 4) must
+match the dense oracle (Eq. 1) to the accuracy eps allows."""
+import numpy as np
+import pytest
+
+from oracle import dense as od
+from synthetic import uniform_iid, standard_normal, perturbed_mesh
+from plan_interp import Plan, Interp
+
+
+def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2):
+    from paper_1709_04419_b200 import Tree
+    t = Tree(pts, leaf, eta)
+    path = str(tmp_path / "plan.bin")
+    t.plan_dump(path, kmax)
+    P = Plan(path)
+    perm = t.perm()
+    I = Interp(P, eps, seed=seed)
+    I.assemble(pts[perm], theta)
+    I.run(P.chol)
+    assert I.fail == 0
+    z = standard_normal(len(pts), k, seed=5)
+    ll, ld, q = I.loglik(z[perm])
+    oll, old, oq = od.loglik(pts, z, theta)
+    return ll, ld, q, oll, old, oq, I, perm
+
+
+@pytest.mark.parametrize("n,leaf,eta,eps,seed", [(300, 16, 2.0, 1e-10, 0), (1024, 8, 3.0, 1e-10, 1),
+                                                 (777, 16, 1.0, 1e-10, 2), (1000, 32, 2.0, 1e-10, 3)])
+def test_planner_matches_dense_oracle(tmp_path, n, leaf, eta, eps, seed):
+    pts = uniform_iid(n, seed)
+    ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), leaf, eta, eps, seed=seed)
+    np.testing.assert_allclose(ll, oll, rtol=1e-8)
+    assert abs(ld - old) <= 1e-6 * abs(old) + 1e-6
+
+
+def test_planner_general_nu_mesh(tmp_path):
+    pts = perturbed_mesh(24, 0.4, seed=4)
+    ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.3, 0.2, 1.5), 16, 2.0, 1e-10)
+    # smooth field (nu = 3/2, ell = 0.2): C is badly conditioned, error ~ eps * cond
+    np.testing.assert_allclose(ll, oll, rtol=1e-6)
+
+
+def test_planner_error_scales_with_eps(tmp_path):
+    pts = uniform_iid(1024, 7)
+    errs = []
+    for eps in (1e-4, 1e-7, 1e-10):
+        ll, _, _, oll, _, _, _, _ = _run(tmp_path, pts, (1.0, 0.1, 0.5), 8, 3.0, eps)
+        errs.append(np.max(np.abs(ll - oll) / np.abs(oll)))
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] < 1e-9
+
+
+def test_sampler_plan_is_L_times_x(tmp_path):
+    # lmul phase computes L~ x; with eps tiny, (L~ x) solved back by the solve phase gives x
+    pts = uniform_iid(500, 9)
+    from paper_1709_04419_b200 import Tree
+    t = Tree(pts, 16, 2.0)
+    path = str(tmp_path / "plan.bin")
+    t.plan_dump(path, 64)
+    P = Plan(path)
+    perm = t.perm()
+    I = Interp(P, 1e-12, seed=1)
+    I.assemble(pts[perm], (1.0, 0.1, 0.5))
+    I.run(P.chol)
+    x = standard_normal(500, 3, seed=2)
+    y = I.lmul(x)
+    # y y^T ~ C in expectation; exact check: L^{-1} y == x
+    I.pool[P.z_off:P.z_off + 500 * P.zw] = 0
+    buf = np.zeros((500, P.zw)); buf[:, :3] = y
+    I.pool[P.z_off:P.z_off + 500 * P.zw] = buf.ravel(order="F")
+    I.run(P.solve)
+    back = I.pool[P.z_off:P.z_off + 500 * P.zw].reshape(P.zw, 500).T[:, :3]
+    np.testing.assert_allclose(back, x, rtol=1e-9, atol=1e-9)
+    # and L~ L~^T == C (dense oracle) through y = L e_j columns
+    C = od.covariance(pts[perm], (1.0, 0.1, 0.5))
+    E = np.zeros((500, 40)); E[np.arange(40), np.arange(40)] = 1.0
+    Lcols = np.concatenate([I.lmul(E[:, i:i + 20]) for i in (0, 20)], axis=1)
+    np.testing.assert_allclose(Lcols[:40, :40] @ Lcols[:40, :40].T, C[:40, :40], atol=1e-9)
+
+
+def test_plan_summary_counts():
+    from paper_1709_04419_b200 import Tree
+    s = Tree(uniform_iid(2000, 0), 32, 2.0).plan_summary(64)
+    assert s["chol_waves"] > 0 and s["chol_vm_tasks"] > 0 and s["solve_tasks"] > 0
+
+
+def test_unsupported_mixed_depth():
+    from paper_1709_04419_b200 import Tree, HMError
+    # 99 points, leaf 32: sizes 49/50 -> 24/25 ... leaves at one depth; 65 points, leaf 32: 32 | 33 -> mixed
+    t = Tree(uniform_iid(65, 0), 32, 2.0)
+    with pytest.raises(HMError):
+        t.plan_summary(64)
