@@ -152,6 +152,20 @@ int hm_stats(hm_handle h, double st[12]);
  * milliseconds (CUDA events on the handle's stream): ms[0..2].              */
 int hm_timings(hm_handle h, double ms[3]);
 
+/* Profiling (measurement support, bench.py).  hm_profile(h, 1) resets the
+ * per-kernel accumulators and brackets every subsequent kernel launch of the
+ * handle with a CUDA event pair on the handle's stream; hm_profile(h, 0)
+ * stops recording.  Both synchronise the handle's stream.                   */
+int hm_profile(hm_handle h, int32_t enable);
+
+/* Per kernel family f = 0..4 (dense Matern block generation, ACA, low-rank
+ * truncation, tile VM, auxiliary gather/finish): out[4f + 0] launches since
+ * the last hm_profile, out[4f + 1] summed device milliseconds of those
+ * launches (0 when profiling is off), out[4f + 2] algorithmic flops (kernel
+ * evaluations for f = 0), out[4f + 3] algorithmic bytes, both counted by the
+ * kernels themselves from their actual dimensions.       */
+int hm_kernel_stats(hm_handle h, double out[20]);
+
 /* ---- dense fp64 check path (n <= 16384) --------------------------------- */
 /* Exact Eq. (1) on the GPU with dense Matern assembly, dense blocked
  * Cholesky, log det and forward solve; out[3*j+0..2] as in hm_loglik.

@@ -72,8 +72,12 @@ __device__ int block_argmax(double v, int idx, double* best, double* sv, int* si
 
 // ---------------------------------------------------------------- assembly
 __global__ void k_dense_gen(const DenseGenTask* __restrict__ tasks, const double* __restrict__ pts,
-                            double* __restrict__ pool, const MaternParams p) {
+                            double* __restrict__ pool, const MaternParams p, double* __restrict__ ctr) {
     const DenseGenTask t = tasks[blockIdx.x];
+    if (threadIdx.x == 0) {   // algorithmic work: m q kernel evaluations, m q doubles written
+        atomicAdd(ctr + CTR_DGEN + 0, (double)t.m * t.q);
+        atomicAdd(ctr + CTR_DGEN + 1, 8.0 * t.m * t.q);
+    }
     double* D = pool + t.off;
     const int tot = t.m * t.q;
     for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
@@ -92,7 +96,8 @@ constexpr int ACA_MAXK = 1024;
 // ||u_k|| ||v_k|| <= eps ||S_k||_F, ||S_k||_F^2 updated incrementally.
 __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__ tasks, const double* __restrict__ pts,
                                                      double* __restrict__ pool, int* __restrict__ ranks,
-                                                     int* __restrict__ flags, const MaternParams p, double eps) {
+                                                     int* __restrict__ flags, const MaternParams p, double eps,
+                                                     double* __restrict__ ctr) {
     const AcaTask t = tasks[blockIdx.x];
     double* U = pool + t.u_off;
     double* V = pool + t.v_off;
@@ -194,7 +199,14 @@ __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__
         istar = inext;
         if (k == cap && threadIdx.x == 0) atomicOr(flags + 1, 1);
     }
-    if (threadIdx.x == 0) ranks[t.rslot] = k;
+    if (threadIdx.x == 0) {
+        ranks[t.rslot] = k;
+        // algorithmic work of k ACA steps: (m + q) kernel evaluations per step plus the
+        // residual updates sum_l 2 l (m + q); bytes: the k (m + q) factor entries written
+        const double kk = (double)k;
+        atomicAdd(ctr + CTR_ACA + 0, kk * (m + q) + kk * (kk - 1.0) * (m + q));
+        atomicAdd(ctr + CTR_ACA + 1, 8.0 * kk * (m + q));
+    }
 }
 
 // ---------------------------------------------------------------- truncation
@@ -321,7 +333,7 @@ __device__ void jacobi_svd(double* X, int rows, int n, double* Z, int* s_flag) {
 
 __global__ void __launch_bounds__(TR_THREADS) k_trunc(const TTask* __restrict__ tasks, const TPiece* __restrict__ pieces,
                                                       double* __restrict__ pool, int* __restrict__ ranks,
-                                                      int* __restrict__ flags, double eps) {
+                                                      int* __restrict__ flags, double eps, double* __restrict__ ctr) {
     const TTask t = tasks[blockIdx.x];
     __shared__ double scratch[32];
     __shared__ int s_flag;
@@ -422,17 +434,31 @@ __global__ void __launch_bounds__(TR_THREADS) k_trunc(const TTask* __restrict__ 
     __syncthreads();
     house_apply_q(A, m, Ka, tauA, Uo, r);
     house_apply_q(Bm, q, Kb, tauB, Vo, r);
-    if (threadIdx.x == 0) ranks[t.rslot] = r;
+    if (threadIdx.x == 0) {
+        ranks[t.rslot] = r;
+        // algorithmic work: Householder QR of the m x K and q x K
+        // stacks, the Ka x Kb core R_A R_B^T, one Jacobi sweep-equivalent per column
+        // pair (counted as one sweep: 6 (Ka + Kb) per pair), and Q_A, Q_B applied
+        // to the r kept columns; bytes: the K (m + q) piece entries read and the
+        // r (m + q) factor entries written.
+        const double Kd = K, md = m, qd = q, ka = Ka, kb = Kb, rd = r;
+        const double fl = 2.0 * (md * Kd * Kd - Kd * Kd * Kd / 3.0) + 2.0 * (qd * Kd * Kd - Kd * Kd * Kd / 3.0) +
+                          2.0 * ka * kb * Kd / 3.0 + 3.0 * kb * (kb - 1.0) * (ka + kb) +
+                          4.0 * md * ka * rd + 4.0 * qd * kb * rd;
+        atomicAdd(ctr + CTR_TRUNC + 0, fl);
+        atomicAdd(ctr + CTR_TRUNC + 1, 8.0 * (Kd * (md + qd) + rd * (md + qd)));
+    }
 }
 
 // ---------------------------------------------------------------- tile VM
 __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks, const VIns* __restrict__ ins,
                                                  double* __restrict__ pool, const int* __restrict__ ranks,
-                                                 int* __restrict__ flags) {
+                                                 int* __restrict__ flags, double* __restrict__ ctr) {
     extern __shared__ double sm[];
     __shared__ int trows[NTILE], tcols[NTILE];
     __shared__ double s_log;
     const VTask task = tasks[blockIdx.x];
+    double c_fl = 0.0, c_by = 0.0;   // algorithmic flops / bytes of this program (thread 0)
     for (int pc = 0; pc < task.ins_count; ++pc) {
         const VIns I = ins[task.ins_begin + pc];
         double* T0 = sm + (int)I.t0 * TSZ;
@@ -440,12 +466,13 @@ __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks
             case VM_LD: {
                 const int r = dim_eval(I.rows, ranks), c = dim_eval(I.cols, ranks);
                 tile_load(T0, pool + I.goff, I.ld, r, c);
-                if (threadIdx.x == 0) { trows[I.t0] = r; tcols[I.t0] = c; }
+                if (threadIdx.x == 0) { trows[I.t0] = r; tcols[I.t0] = c; c_by += 8.0 * r * c; }
                 __syncthreads();
             } break;
             case VM_ST: {
                 const int r = dim_eval(I.rows, ranks), c = dim_eval(I.cols, ranks);
                 tile_store(T0, pool + I.goff, I.ld, min(r, trows[I.t0]), min(c, tcols[I.t0]));
+                if (threadIdx.x == 0) c_by += 8.0 * min(r, trows[I.t0]) * min(c, tcols[I.t0]);
                 __syncthreads();
             } break;
             case VM_ZERO: {
@@ -469,11 +496,13 @@ __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks
                     __syncthreads();
                     if (threadIdx.x == 0) { trows[I.t0] = m; tcols[I.t0] = n; }
                 }
+                if (threadIdx.x == 0) c_fl += 2.0 * m * n * k;
                 if (m > 0 && n > 0 && k > 0)
                     tile_gemm(T0, T1, I.ta != 0, T2, I.tb != 0, m, n, k, I.alpha, I.beta == 0.0 ? 0.0 : I.beta);
                 __syncthreads();
             } break;
             case VM_POTRF: {
+                if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * trows[I.t0] * trows[I.t0] / 3.0;
                 const int f = tile_potrf(T0, trows[I.t0], &s_log);
                 if (threadIdx.x == 0) {
                     pool[I.goff] = s_log;
@@ -482,17 +511,24 @@ __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks
                 __syncthreads();
             } break;
             case VM_TRSM_RLT: {
+                if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * tcols[I.t0] * tcols[I.t0];
                 tile_trsm_rlt(T0, sm + (int)I.t1 * TSZ, trows[I.t0], tcols[I.t0]);
             } break;
             case VM_TRSM_LN: {
+                if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * trows[I.t0] * tcols[I.t0];
                 tile_trsm_ln(T0, sm + (int)I.t1 * TSZ, trows[I.t0], tcols[I.t0]);
             } break;
             case VM_TRMM_LN: {
+                if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * trows[I.t0] * tcols[I.t0];
                 tile_trmm_ln(T0, sm + (int)I.t1 * TSZ, trows[I.t0], tcols[I.t0]);
             } break;
             default:
                 break;
         }
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(ctr + CTR_VM + 0, c_fl);
+        atomicAdd(ctr + CTR_VM + 1, c_by);
     }
 }
 
@@ -538,16 +574,16 @@ __global__ void k_finish(const double* __restrict__ logd, int nleaves, const dou
 
 // ---------------------------------------------------------------- host launchers
 void launch_dense_gen(const DenseGenTask* t, int n, const double* pts, double* pool, const MaternParams& p,
-                      cudaStream_t st) {
-    if (n > 0) k_dense_gen<<<n, 256, 0, st>>>(t, pts, pool, p);
+                      double* ctr, cudaStream_t st) {
+    if (n > 0) k_dense_gen<<<n, 256, 0, st>>>(t, pts, pool, p, ctr);
 }
 void launch_aca(const AcaTask* t, int n, const double* pts, double* pool, int* ranks, int* flags,
-                const MaternParams& p, double eps, cudaStream_t st) {
-    if (n > 0) k_aca<<<n, ACA_THREADS, 0, st>>>(t, pts, pool, ranks, flags, p, eps);
+                const MaternParams& p, double eps, double* ctr, cudaStream_t st) {
+    if (n > 0) k_aca<<<n, ACA_THREADS, 0, st>>>(t, pts, pool, ranks, flags, p, eps, ctr);
 }
 void launch_trunc(const TTask* t, int n, const TPiece* pc, double* pool, int* ranks, int* flags, double eps,
-                  cudaStream_t st) {
-    if (n > 0) k_trunc<<<n, TR_THREADS, 0, st>>>(t, pc, pool, ranks, flags, eps);
+                  double* ctr, cudaStream_t st) {
+    if (n > 0) k_trunc<<<n, TR_THREADS, 0, st>>>(t, pc, pool, ranks, flags, eps, ctr);
 }
 void vm_set_attr() {
     static bool done = false;
@@ -555,8 +591,9 @@ void vm_set_attr() {
     HM_CUDA_TRY(cudaFuncSetAttribute(k_vm, cudaFuncAttributeMaxDynamicSharedMemorySize, NTILE * TSZ * 8));
     done = true;
 }
-void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, cudaStream_t st) {
-    if (n > 0) k_vm<<<n, TTHREADS, NTILE * TSZ * 8, st>>>(t, ins, pool, ranks, flags);
+void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, double* ctr,
+               cudaStream_t st) {
+    if (n > 0) k_vm<<<n, TTHREADS, NTILE * TSZ * 8, st>>>(t, ins, pool, ranks, flags, ctr);
 }
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st) {
     const int64_t tot = n * zw;

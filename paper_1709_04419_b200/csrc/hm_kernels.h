@@ -5,14 +5,18 @@
 #include "hm_tasks.h"
 
 namespace hm {
+// Device work counters (doubles): [CTR_x + 0] algorithmic flops (or kernel
+// evaluations for DGEN), [CTR_x + 1] algorithmic bytes, accumulated by the kernels.
+constexpr int CTR_DGEN = 0, CTR_ACA = 2, CTR_TRUNC = 4, CTR_VM = 6, CTR_N = 8;
 void launch_dense_gen(const DenseGenTask* t, int n, const double* pts, double* pool, const MaternParams& p,
-                      cudaStream_t st);
+                      double* ctr, cudaStream_t st);
 void launch_aca(const AcaTask* t, int n, const double* pts, double* pool, int* ranks, int* flags,
-                const MaternParams& p, double eps, cudaStream_t st);
+                const MaternParams& p, double eps, double* ctr, cudaStream_t st);
 void launch_trunc(const TTask* t, int n, const TPiece* pc, double* pool, int* ranks, int* flags, double eps,
-                  cudaStream_t st);
+                  double* ctr, cudaStream_t st);
 void vm_set_attr();
-void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, cudaStream_t st);
+void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, double* ctr,
+               cudaStream_t st);
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st);
 void launch_scatter(const double* Zt, const int64_t* perm, int64_t n, int kz, double* Z, cudaStream_t st);
 void launch_finish(const double* logd, int nleaves, const double* Zt, int64_t n, int kz, double* out,

@@ -23,6 +23,8 @@
 
 namespace hm {
 
+enum KFamily { KF_DGEN = 0, KF_ACA = 1, KF_TRUNC = 2, KF_VM = 3, KF_AUX = 4, KF_N = 5 };
+
 struct DPhase {
     DevBuf ins, vt, tt, tp;
     const Phase* ph = nullptr;
@@ -41,7 +43,13 @@ struct hm_handle_s {
     hm_params prm{};
     hm_theta theta{};
     MaternParams mp{};
-    DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca;
+    DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca, ctr;
+    // profiling: per kernel family (KF_*) launch counts (always) and, when
+    // enabled, a CUDA event pair around every launch on the handle's stream
+    bool profiling = false;
+    int64_t launches[KF_N] = {0, 0, 0, 0, 0};
+    std::vector<cudaEvent_t> evpool;
+    std::vector<std::pair<int, int>> evlog;   // (family, index of first event of the pair)
     DPhase rec, chol, solve, lmul;
     bool assembled = false, factored = false;
     cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -50,6 +58,8 @@ struct hm_handle_s {
     std::vector<int> h_ranks;
     ~hm_handle_s() {
         for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : evpool)
             if (e) cudaEventDestroy(e);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
@@ -71,17 +81,47 @@ void upload_phase(DPhase& d, const Phase& p, cudaStream_t st) {
     d.ph = &p;
 }
 
+// Profiling bracket around one launch of kernel family f.
+struct Launch {
+    hm_handle_s* h;
+    int f;
+    int idx = -1;
+    Launch(hm_handle_s* hh, int fam) : h(hh), f(fam) {
+        ++h->launches[f];
+        if (!h->profiling) return;
+        idx = (int)(2 * h->evlog.size());
+        while ((int)h->evpool.size() < idx + 2) {
+            cudaEvent_t e;
+            HM_CUDA_TRY(cudaEventCreate(&e));
+            h->evpool.push_back(e);
+        }
+        HM_CUDA_TRY(cudaEventRecord(h->evpool[idx], h->stream));
+    }
+    ~Launch() {
+        if (idx < 0) return;
+        cudaEventRecord(h->evpool[idx + 1], h->stream);
+        h->evlog.push_back({f, idx});
+    }
+};
+
 void run_phase(hm_handle_s* h, const DPhase& d) {
     const Phase& p = *d.ph;
     double* pool = h->pool.as<double>();
     int* ranks = h->ranks.as<int>();
     int* flags = h->flags.as<int>();
+    double* ctr = h->ctr.as<double>();
     for (int w = 0; w < p.nwaves; ++w) {
         const int v0 = p.v_wave_begin[w], v1 = p.v_wave_begin[w + 1];
         const int t0 = p.t_wave_begin[w], t1 = p.t_wave_begin[w + 1];
-        if (t1 > t0)
-            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->prm.eps, h->stream);
-        if (v1 > v0) launch_vm(d.vt.as<VTask>() + v0, v1 - v0, d.ins.as<VIns>(), pool, ranks, flags, h->stream);
+        if (t1 > t0) {
+            Launch L(h, KF_TRUNC);
+            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->prm.eps, ctr,
+                         h->stream);
+        }
+        if (v1 > v0) {
+            Launch L(h, KF_VM);
+            launch_vm(d.vt.as<VTask>() + v0, v1 - v0, d.ins.as<VIns>(), pool, ranks, flags, ctr, h->stream);
+        }
     }
     HM_CUDA_TRY(cudaGetLastError());
 }
@@ -114,11 +154,17 @@ void do_assemble(hm_handle_s* h, hm_theta th) {
     matern_setup(th.sigma2, th.ell, th.nu, h->mp);
     HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
     HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
-    launch_dense_gen(h->dgen.as<DenseGenTask>(), (int)h->P.dgen.size(), h->pts.as<double>(), h->pool.as<double>(),
-                     h->mp, h->stream);
+    {
+        Launch L(h, KF_DGEN);
+        launch_dense_gen(h->dgen.as<DenseGenTask>(), (int)h->P.dgen.size(), h->pts.as<double>(),
+                         h->pool.as<double>(), h->mp, h->ctr.as<double>(), h->stream);
+    }
     // ACA at eps/4, then recompression to eps (QR + SVD)
-    launch_aca(h->aca.as<AcaTask>(), (int)h->P.aca.size(), h->pts.as<double>(), h->pool.as<double>(),
-               h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->prm.eps, h->stream);
+    {
+        Launch L(h, KF_ACA);
+        launch_aca(h->aca.as<AcaTask>(), (int)h->P.aca.size(), h->pts.as<double>(), h->pool.as<double>(),
+                   h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->prm.eps, h->ctr.as<double>(), h->stream);
+    }
     run_phase(h, h->rec);
     HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
     int f[4];
@@ -165,9 +211,16 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
                                         h->stream));
             src = h->zio.as<double>();
         }
-        launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+        {
+            Launch L(h, KF_AUX);
+            launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+        }
         run_phase(h, h->solve);
-        launch_finish(h->pool.as<double>() + h->P.logd_off, h->P.n_leaves, zt, n, kc, h->out.as<double>(), h->stream);
+        {
+            Launch L(h, KF_AUX);
+            launch_finish(h->pool.as<double>() + h->P.logd_off, h->P.n_leaves, zt, n, kc, h->out.as<double>(),
+                          h->stream);
+        }
         HM_CUDA_TRY(cudaMemcpyAsync(out_host + 3 * c0, h->out.p, sizeof(double) * 3 * kc, cudaMemcpyDeviceToHost,
                                     h->stream));
     }
@@ -220,6 +273,8 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         h->ranks.alloc(sizeof(int) * (h->P.n_slots + 1));
         HM_CUDA_TRY(cudaMemsetAsync(h->ranks.p, 0, sizeof(int) * (h->P.n_slots + 1), h->stream));
         h->flags.alloc(sizeof(int) * 4);
+        h->ctr.alloc(sizeof(double) * CTR_N);
+        HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
         h->out.alloc(sizeof(double) * 3 * h->P.zw);
         upload(h->dgen, h->P.dgen, h->stream);
         upload(h->aca, h->P.aca, h->stream);
@@ -379,6 +434,48 @@ int hm_stats(hm_handle h, double st[12]) {
         st[9] = P.chol.nwaves;
         st[10] = (double)P.chol.n_launches();
         st[11] = 0;
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_profile(hm_handle h, int32_t enable) {
+    try {
+        if (!h) throw ApiError(HM_ERR_ARG, "null handle");
+        DeviceGuard dg(h->device);
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        h->profiling = enable != 0;
+        h->evlog.clear();
+        for (auto& x : h->launches) x = 0;
+        HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_kernel_stats(hm_handle h, double out[20]) {
+    try {
+        if (!h || !out) throw ApiError(HM_ERR_ARG, "null pointer");
+        DeviceGuard dg(h->device);
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        double ms[KF_N] = {0, 0, 0, 0, 0};
+        for (auto& e : h->evlog) {
+            float t = 0;
+            HM_CUDA_TRY(cudaEventElapsedTime(&t, h->evpool[e.second], h->evpool[e.second + 1]));
+            ms[e.first] += t;
+        }
+        double c[CTR_N];
+        HM_CUDA_TRY(cudaMemcpy(c, h->ctr.p, sizeof(double) * CTR_N, cudaMemcpyDeviceToHost));
+        const int cmap[KF_N] = {CTR_DGEN, CTR_ACA, CTR_TRUNC, CTR_VM, -1};
+        for (int f = 0; f < KF_N; ++f) {
+            out[4 * f + 0] = (double)h->launches[f];
+            out[4 * f + 1] = ms[f];
+            out[4 * f + 2] = cmap[f] >= 0 ? c[cmap[f]] : 0.0;
+            out[4 * f + 3] = cmap[f] >= 0 ? c[cmap[f] + 1] : 0.0;
+        }
         return HM_OK;
     } catch (...) {
         return translate_exception();
