@@ -59,7 +59,7 @@ typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
 /* H-matrix parameters.  eps: relative accuracy per admissible block (Remark 2,
  * l.166, adaptive-rank strategy; reading R4); leaf: n_min (l.211);
  * eta: admissibility parameter (reading R2); kmax: rank capacity of one
- * low-rank block (HM_ERR_RANK_CAP when exceeded; 0 = default 160).            */
+ * low-rank block, at most 240 (HM_ERR_RANK_CAP when exceeded; 0 = default 160). */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
@@ -145,7 +145,8 @@ int hm_matvec(hm_handle h, const double* x, int32_t x_on_device, int32_t k,
 
 /* Statistics.  st[0..11]: n, #dense blocks, #low-rank blocks, max rank C~,
  * max rank L~, bytes C~, bytes L~, compression ratio C~ (1 - bytes/8n^2),
- * #plan tasks, #plan waves, #kernel launches per Cholesky, rank-cap flag.   */
+ * #plan tasks, #plan waves, #kernel launches per Cholesky, widest Cholesky
+ * truncation (sum of the actual widths of its stacked pieces).             */
 int hm_stats(hm_handle h, double st[12]);
 
 /* Timing of the last hm_assemble / hm_cholesky / hm_loglik on the device,

@@ -242,7 +242,7 @@ class HMatrix:
         s = np.zeros(12)
         check(lib.hm_stats(self._h, s.ctypes.data_as(C.c_void_p)))
         keys = ("n", "dense_blocks", "lowrank_blocks", "max_rank_C", "max_rank_L", "bytes_C", "bytes_L",
-                "compression_C", "chol_tasks", "chol_waves", "chol_launches", "reserved")
+                "compression_C", "chol_tasks", "chol_waves", "chol_launches", "max_trunc_width")
         return dict(zip(keys, s.tolist()))
 
     def timings(self) -> dict:

@@ -1,10 +1,7 @@
 // Device kernels of the H-matrix path (sec. 2-3):
 //   k_dense_gen  -- Matern entries of dense (inadmissible / leaf-pair) blocks      Eq. (2)
 //   k_aca        -- partially pivoted ACA of admissible blocks to accuracy eps      l.147
-//   k_trunc      -- truncation of an accumulated low-rank sum: Householder QR of
-//                   both factors, one-sided Jacobi SVD of the small core, keep
-//                   sigma_i > eps * sigma_1 (adaptive-rank strategy, Remark 2 l.166;
-//                   "efficient rank-truncation techniques", l.87)
+//   (k_trunc, the low-rank truncation, lives in trunc.cu)
 //   k_vm         -- tile VM: leaf-level POTRF / TRSM / products on 64 x 64 fp64
 //                   shared-memory tiles with FP64 tensor-core MMA (see tile.cuh)
 //   k_gather / k_scatter / k_finish -- permutation to tree order, log det
@@ -19,56 +16,9 @@
 #include "hm_tasks.h"
 #include "matern.cuh"
 #include "tile.cuh"
+#include "dev_util.cuh"
 
 namespace hm {
-
-__device__ __forceinline__ int dim_eval(const Dim& d, const int* __restrict__ ranks) {
-    if (d.slot < 0) return d.stat;
-    int v = ranks[d.slot] - d.off;
-    return v < 0 ? 0 : (v > d.stat ? d.stat : v);
-}
-
-// ---------------------------------------------------------------- reductions
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// block-wide sum (all threads get the result); scratch >= 32 doubles
-__device__ double block_sum(double v, double* scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_sum(v);
-    __syncthreads();
-    if (lane == 0) scratch[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int i = 0; i < nw; ++i) s += scratch[i];
-    __syncthreads();
-    return s;
-}
-
-// block-wide argmax of |v| (ties -> smaller index); returns index, *best = value
-__device__ int block_argmax(double v, int idx, double* best, double* sv, int* si) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double a = fabs(v);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        double a2 = __shfl_xor_sync(0xffffffffu, a, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-        if (a2 > a || (a2 == a && i2 < idx)) { a = a2; idx = i2; }
-    }
-    __syncthreads();
-    if (lane == 0) { sv[warp] = a; si[warp] = idx; }
-    __syncthreads();
-    double ba = -1.0;
-    int bi = 0x7fffffff;
-    for (int i = 0; i < nw; ++i)
-        if (sv[i] > ba || (sv[i] == ba && si[i] < bi)) { ba = sv[i]; bi = si[i]; }
-    __syncthreads();
-    *best = ba;
-    return bi;
-}
 
 // ---------------------------------------------------------------- assembly
 __global__ void k_dense_gen(const DenseGenTask* __restrict__ tasks, const double* __restrict__ pts,
@@ -209,247 +159,6 @@ __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__
     }
 }
 
-// ---------------------------------------------------------------- truncation
-constexpr int TR_THREADS = 256;
-
-// Householder QR of A (m x K, ld m) in place; tau[K].  R in the upper triangle.
-__device__ void house_qr(double* A, int m, int K, double* tau, double* scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int kmin = min(m, K);
-    __shared__ double s_beta, s_scale, s_tau;
-    for (int i = 0; i < kmin; ++i) {
-        double* a = A + (int64_t)i * m;
-        double ss = 0.0;
-        for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) ss += a[r] * a[r];
-        const double sig = block_sum(ss, scratch);
-        if (threadIdx.x == 0) {
-            const double alpha = a[i];
-            if (sig == 0.0) {
-                s_tau = 0.0;
-                s_scale = 0.0;
-                s_beta = alpha;
-            } else {
-                const double nrm = sqrt(alpha * alpha + sig);
-                const double beta = (alpha <= 0.0) ? nrm : -nrm;
-                s_tau = (beta - alpha) / beta;
-                s_scale = 1.0 / (alpha - beta);
-                s_beta = beta;
-            }
-            tau[i] = s_tau;
-        }
-        __syncthreads();
-        const double tv = s_tau, sc = s_scale;
-        if (tv != 0.0)
-            for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) a[r] *= sc;
-        __syncthreads();
-        if (threadIdx.x == 0) a[i] = s_beta;
-        __syncthreads();
-        if (tv != 0.0) {
-            // apply H = I - tau v v^T (v_i = 1) to columns c > i: one warp per column
-            for (int c = i + 1 + warp; c < K; c += nw) {
-                double* col = A + (int64_t)c * m;
-                double w = (lane == 0) ? col[i] : 0.0;
-                for (int r = i + 1 + lane; r < m; r += 32) w += a[r] * col[r];
-                w = warp_sum(w) * tv;
-                if (lane == 0) col[i] -= w;
-                for (int r = i + 1 + lane; r < m; r += 32) col[r] -= w * a[r];
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Y (m x r, ld m) <- Q Y with Q = H_0 H_1 ... H_{kmin-1} stored in A (m x K) / tau
-__device__ void house_apply_q(const double* A, int m, int kmin, const double* tau, double* Y, int r) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = kmin - 1; i >= 0; --i) {
-        const double tv = tau[i];
-        if (tv == 0.0) continue;
-        const double* a = A + (int64_t)i * m;
-        for (int c = warp; c < r; c += nw) {
-            double* col = Y + (int64_t)c * m;
-            double w = (lane == 0) ? col[i] : 0.0;
-            for (int rr = i + 1 + lane; rr < m; rr += 32) w += a[rr] * col[rr];
-            w = warp_sum(w) * tv;
-            if (lane == 0) col[i] -= w;
-            for (int rr = i + 1 + lane; rr < m; rr += 32) col[rr] -= w * a[rr];
-        }
-        __syncthreads();
-    }
-}
-
-// one-sided Jacobi: X (rows x n, ld rows) -> X Z with orthogonal columns; Z (n x n, ld n)
-__device__ void jacobi_svd(double* X, int rows, int n, double* Z, int* s_flag) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Z[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
-    __syncthreads();
-    if (n < 2) return;
-    const int nn = (n + 1) & ~1;   // even number of players (one dummy if n odd)
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        if (threadIdx.x == 0) *s_flag = 0;
-        __syncthreads();
-        for (int round = 0; round < nn - 1; ++round) {
-            for (int pr = warp; pr < nn / 2; pr += nw) {
-                // round-robin pairing: player 0 fixed, others rotate
-                int a = (pr == 0) ? 0 : ((round + pr - 1) % (nn - 1)) + 1;
-                int b = ((round + nn - 2 - pr) % (nn - 1)) + 1;
-                if (pr == 0) b = ((round + nn - 2) % (nn - 1)) + 1;
-                if (a >= n || b >= n) continue;
-                if (a > b) { int tmp = a; a = b; b = tmp; }
-                double* xa = X + (int64_t)a * rows;
-                double* xb = X + (int64_t)b * rows;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int r = lane; r < rows; r += 32) {
-                    const double u = xa[r], v = xb[r];
-                    al += u * u; be += v * v; ga += u * v;
-                }
-                al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-                if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
-                    const double zeta = (be - al) / (2.0 * ga);
-                    const double tt = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-                    for (int r = lane; r < rows; r += 32) {
-                        const double u = xa[r], v = xb[r];
-                        xa[r] = c * u - s * v;
-                        xb[r] = s * u + c * v;
-                    }
-                    double* za = Z + (int64_t)a * n;
-                    double* zb = Z + (int64_t)b * n;
-                    for (int r = lane; r < n; r += 32) {
-                        const double u = za[r], v = zb[r];
-                        za[r] = c * u - s * v;
-                        zb[r] = s * u + c * v;
-                    }
-                    if (lane == 0) *s_flag = 1;
-                }
-            }
-            __syncthreads();
-        }
-        if (*s_flag == 0) break;
-        __syncthreads();
-    }
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(TR_THREADS) k_trunc(const TTask* __restrict__ tasks, const TPiece* __restrict__ pieces,
-                                                      double* __restrict__ pool, int* __restrict__ ranks,
-                                                      int* __restrict__ flags, double eps, double* __restrict__ ctr) {
-    const TTask t = tasks[blockIdx.x];
-    __shared__ double scratch[32];
-    __shared__ int s_flag;
-    __shared__ int s_rank;
-    const int m = t.m, q = t.q;
-    // actual widths
-    int K = 0;
-    for (int p = 0; p < t.piece_count; ++p) K += dim_eval(pieces[t.piece_begin + p].w, ranks);
-    double* ws = pool + t.ws;
-    double* A = ws;                       // m x K
-    double* Bm = A + (int64_t)m * K;      // q x K
-    double* tauA = Bm + (int64_t)q * K;   // K
-    double* tauB = tauA + K;              // K
-    double* sig = tauB + K;               // K
-    double* X = sig + K;                  // Ka x Kb  (<= K x K)
-    double* Z = X + (int64_t)K * K;       // Kb x Kb
-    // gather
-    int koff = 0;
-    for (int pi = 0; pi < t.piece_count; ++pi) {
-        const TPiece pc = pieces[t.piece_begin + pi];
-        const int w = dim_eval(pc.w, ranks);
-        const double* Up = pool + pc.u_off;
-        const double* Vp = pool + pc.v_off;
-        for (int idx = threadIdx.x; idx < m * w; idx += blockDim.x) {
-            const int r = idx % m, c = idx / m;
-            const int rr = r - pc.u_row0;
-            A[(int64_t)(koff + c) * m + r] = (rr >= 0 && rr < pc.u_rows) ? pc.alpha * Up[rr + (int64_t)c * pc.u_ld] : 0.0;
-        }
-        for (int idx = threadIdx.x; idx < q * w; idx += blockDim.x) {
-            const int r = idx % q, c = idx / q;
-            const int rr = r - pc.v_row0;
-            Bm[(int64_t)(koff + c) * q + r] = (rr >= 0 && rr < pc.v_rows) ? Vp[rr + (int64_t)c * pc.v_ld] : 0.0;
-        }
-        koff += w;
-    }
-    __syncthreads();
-    if (K == 0) {
-        if (threadIdx.x == 0) ranks[t.rslot] = 0;
-        return;
-    }
-    house_qr(A, m, K, tauA, scratch);
-    house_qr(Bm, q, K, tauB, scratch);
-    const int Ka = min(m, K), Kb = min(q, K);
-    // X = R_A R_B^T  (Ka x Kb), R_A[i][c] (c >= i) = A[i + c m], R_B[j][c] = Bm[j + c q]
-    for (int idx = threadIdx.x; idx < Ka * Kb; idx += blockDim.x) {
-        const int i = idx % Ka, j = idx / Ka;
-        double s = 0.0;
-        for (int c = max(i, j); c < K; ++c) s += A[i + (int64_t)c * m] * Bm[j + (int64_t)c * q];
-        X[i + (int64_t)j * Ka] = s;
-    }
-    __syncthreads();
-    jacobi_svd(X, Ka, Kb, Z, &s_flag);
-    // singular values = column norms of X
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = warp; j < Kb; j += nw) {
-        double s = 0.0;
-        for (int r = lane; r < Ka; r += 32) s += X[r + (int64_t)j * Ka] * X[r + (int64_t)j * Ka];
-        s = warp_sum(s);
-        if (lane == 0) sig[j] = sqrt(s);
-    }
-    __syncthreads();
-    // order by decreasing sigma (rank counting, ties by index), rank by eps * sigma_max
-    __shared__ int order[ACA_MAXK];
-    __shared__ double s_smax;
-    const int kk = min(Kb, ACA_MAXK);
-    for (int j = threadIdx.x; j < kk; j += blockDim.x) {
-        int pos = 0;
-        const double sj = sig[j];
-        for (int b = 0; b < kk; ++b) pos += (sig[b] > sj || (sig[b] == sj && b < j)) ? 1 : 0;
-        order[pos] = j;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_smax = (kk > 0) ? sig[order[0]] : 0.0;
-    __syncthreads();
-    {
-        int cnt = 0;
-        for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (sig[j] > eps * s_smax && sig[j] > 0.0) ? 1 : 0;
-        const double tot = block_sum((double)cnt, scratch);
-        if (threadIdx.x == 0) {
-            int r = (int)(tot + 0.5);
-            if (r > t.cap) { atomicOr(flags + 1, 2); r = t.cap; }
-            s_rank = r;
-        }
-    }
-    __syncthreads();
-    const int r = s_rank;
-    // U_out = Q_A [X(:, order) ; 0],  V_out = Q_B [Z(:, order) ; 0]
-    double* Uo = pool + t.u_out;
-    double* Vo = pool + t.v_out;
-    for (int idx = threadIdx.x; idx < m * r; idx += blockDim.x) {
-        const int i = idx % m, c = idx / m;
-        Uo[i + (int64_t)c * m] = (i < Ka) ? X[i + (int64_t)order[c] * Ka] : 0.0;
-    }
-    for (int idx = threadIdx.x; idx < q * r; idx += blockDim.x) {
-        const int i = idx % q, c = idx / q;
-        Vo[i + (int64_t)c * q] = (i < Kb) ? Z[i + (int64_t)order[c] * Kb] : 0.0;
-    }
-    __syncthreads();
-    house_apply_q(A, m, Ka, tauA, Uo, r);
-    house_apply_q(Bm, q, Kb, tauB, Vo, r);
-    if (threadIdx.x == 0) {
-        ranks[t.rslot] = r;
-        // algorithmic work: Householder QR of the m x K and q x K
-        // stacks, the Ka x Kb core R_A R_B^T, one Jacobi sweep-equivalent per column
-        // pair (counted as one sweep: 6 (Ka + Kb) per pair), and Q_A, Q_B applied
-        // to the r kept columns; bytes: the K (m + q) piece entries read and the
-        // r (m + q) factor entries written.
-        const double Kd = K, md = m, qd = q, ka = Ka, kb = Kb, rd = r;
-        const double fl = 2.0 * (md * Kd * Kd - Kd * Kd * Kd / 3.0) + 2.0 * (qd * Kd * Kd - Kd * Kd * Kd / 3.0) +
-                          2.0 * ka * kb * Kd / 3.0 + 3.0 * kb * (kb - 1.0) * (ka + kb) +
-                          4.0 * md * ka * rd + 4.0 * qd * kb * rd;
-        atomicAdd(ctr + CTR_TRUNC + 0, fl);
-        atomicAdd(ctr + CTR_TRUNC + 1, 8.0 * (Kd * (md + qd) + rd * (md + qd)));
-    }
-}
-
 // ---------------------------------------------------------------- tile VM
 __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks, const VIns* __restrict__ ins,
                                                  double* __restrict__ pool, const int* __restrict__ ranks,
@@ -580,10 +289,6 @@ void launch_dense_gen(const DenseGenTask* t, int n, const double* pts, double* p
 void launch_aca(const AcaTask* t, int n, const double* pts, double* pool, int* ranks, int* flags,
                 const MaternParams& p, double eps, double* ctr, cudaStream_t st) {
     if (n > 0) k_aca<<<n, ACA_THREADS, 0, st>>>(t, pts, pool, ranks, flags, p, eps, ctr);
-}
-void launch_trunc(const TTask* t, int n, const TPiece* pc, double* pool, int* ranks, int* flags, double eps,
-                  double* ctr, cudaStream_t st) {
-    if (n > 0) k_trunc<<<n, TR_THREADS, 0, st>>>(t, pc, pool, ranks, flags, eps, ctr);
 }
 void vm_set_attr() {
     static bool done = false;

@@ -62,8 +62,23 @@ struct TTask {
     int32_t m, q, cap, rslot;
     int32_t piece_begin, piece_count;
     int32_t kmax_tot;         // sum of static piece widths
-    int32_t pad;
+    int32_t wmax;             // largest static piece width
 };
+
+// k_trunc algorithm selection and workspace (trunc.cu; planner sizes the workspace)
+constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs
+constexpr int TR_RB = 16;         // probes per round of the randomized range finder
+constexpr int TR_WMAX_SM = 64;    // piece columns staged per shared-memory chunk
+constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
+inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot, int32_t wmax) {
+    if (kmax_tot <= TR_EXACT_K) {
+        const int64_t K = kmax_tot;
+        return ((int64_t)m + q + 2 * K + 8) * K + 64;
+    }
+    const int64_t L = (int64_t)cap + TR_RB;
+    return (int64_t)q * TR_RB + (int64_t)m * L + (int64_t)m * TR_RB + (int64_t)q * L + (int64_t)wmax * L +
+           2 * L * L + 2 * L + 64;
+}
 
 // ---- assembly ------------------------------------------------------------
 struct DenseGenTask {         // D[i + j m] = C(|x_{r0+i} - x_{c0+j}|), i < m, j < q

@@ -243,7 +243,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (params.leaf < 1 || params.leaf > 64) throw ApiError(HM_ERR_ARG, "1 <= leaf <= 64 required");
         if (!(params.eta > 0.0)) throw ApiError(HM_ERR_ARG, "eta > 0 required");
         if (params.kmax <= 0) params.kmax = 160;
-        if (params.kmax > 1000) throw ApiError(HM_ERR_ARG, "kmax <= 1000 required");
+        if (params.kmax > TR_LMAX - TR_RB) throw ApiError(HM_ERR_ARG, "kmax <= 240 required");
         check_theta(theta);
         DeviceGuard dg(device);
         h = new hm_handle_s();
@@ -433,7 +433,18 @@ int hm_stats(hm_handle h, double st[12]) {
         st[8] = (double)(P.chol.vt.size() + P.chol.tt.size());
         st[9] = P.chol.nwaves;
         st[10] = (double)P.chol.n_launches();
-        st[11] = 0;
+        // widest truncation of the Cholesky at the current ranks (sum of actual piece widths)
+        int kmaxw = 0;
+        for (const TTask& t : P.chol.tt) {
+            int K = 0;
+            for (int p = 0; p < t.piece_count; ++p) {
+                const Dim& d = P.chol.tp[t.piece_begin + p].w;
+                if (d.slot < 0) K += d.stat;
+                else K += std::max(0, std::min(d.stat, h->h_ranks[d.slot] - d.off));
+            }
+            kmaxw = std::max(kmaxw, K);
+        }
+        st[11] = kmaxw;
         return HM_OK;
     } catch (...) {
         return translate_exception();

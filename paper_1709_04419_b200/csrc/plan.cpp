@@ -546,11 +546,14 @@ struct Builder {
         t.m = s.m; t.q = s.p; t.cap = s.cap; t.rslot = s.rslot;
         t.piece_begin = (int32_t)ph->tp.size();
         t.piece_count = (int32_t)pcs.size();
-        int32_t kt = 0;
-        for (auto& p : pcs) kt += p.w.stat;
+        int32_t kt = 0, wmax = 0;
+        for (auto& p : pcs) {
+            kt += p.w.stat;
+            wmax = std::max(wmax, p.w.stat);
+        }
         t.kmax_tot = kt;
-        const int64_t K = kt;
-        t.ws_size = ((int64_t)s.m + s.p + 2 * K + 8) * K + 64;
+        t.wmax = wmax;
+        t.ws_size = trunc_ws_size(s.m, s.p, s.cap, kt, wmax);
         if ((int)ws_arena.size() <= w) ws_arena.resize(w + 1, 0);
         t.ws = ws_arena[w];           // relative; rebased after planning
         ws_arena[w] += (t.ws_size + 31) & ~int64_t(31);

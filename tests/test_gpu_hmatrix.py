@@ -36,17 +36,21 @@ def test_config0(hm, config0, eps, tol):
     assert st["lowrank_blocks"] > 0
 
 
-@pytest.mark.parametrize("n,nu,ell,leaf", [(1500, 1.0, 0.1, 32), (999, 0.35, 0.05, 16), (4096, 1.5, 0.2, 64)])
+@pytest.mark.parametrize("n,nu,ell,leaf", [(1500, 1.0, 0.1, 32), (999, 0.35, 0.05, 16), (4096, 1.5, 0.05, 64),
+                                           (3000, 0.73, 0.0864, 32)])
 def test_general_nu(hm, n, nu, ell, leaf):
+    # Z = L xi drawn from the model (dense oracle factor), 3 replicates
     pts = uniform_iid(n, seed=n)
     theta = (1.2, ell, nu)
-    Z = standard_normal(n, 3, seed=4)
-    oll, old, oq = od.loglik(pts, Z, theta, bessel="quad" if n <= 2000 else "scipy")
+    bessel = "quad" if n <= 2000 else "scipy"
+    C = od.covariance(pts, theta, bessel=bessel)
+    Z = np.linalg.cholesky(C) @ standard_normal(n, 3, seed=4)
+    oll, old, oq = od.loglik_from_cov(C, Z)
     H = hm.HMatrix(pts, theta, eps=1e-8, leaf=leaf, eta=2.0)
     H.cholesky()
     got = H.loglik(Z)
     np.testing.assert_allclose(got[:, 0], oll, rtol=1e-6)
-    assert abs(got[0, 1] - old) <= 1e-6 * abs(oll)
+    assert abs(got[0, 1] - old) <= 1e-6 * float(np.max(np.abs(oll)))
 
 
 def test_tiny_and_single_leaf(hm):
