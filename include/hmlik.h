@@ -159,13 +159,19 @@ int hm_timings(hm_handle h, double ms[3]);
  * stops recording.  Both synchronise the handle's stream.                   */
 int hm_profile(hm_handle h, int32_t enable);
 
-/* Per kernel family f = 0..4 (dense Matern block generation, ACA, low-rank
- * truncation, tile VM, auxiliary gather/finish): out[4f + 0] launches since
+/* Execution mode of the planned phases (Cholesky, solve, sampler, recompression):
+ * 1 (default) = one persistent dependency-driven kernel per phase (k_exec),
+ * 0 = one launch per wave and task type (k_trunc, k_vm).  Same arithmetic.     */
+int hm_set_exec_mode(hm_handle h, int32_t mode);
+
+/* Per kernel family f = 0..5 (dense Matern block generation, ACA, low-rank
+ * truncation, tile VM, auxiliary gather/finish, persistent executor -- whose
+ * flops/bytes are those of the truncation + VM tasks it ran): out[4f + 0] launches since
  * the last hm_profile, out[4f + 1] summed device milliseconds of those
  * launches (0 when profiling is off), out[4f + 2] algorithmic flops (kernel
  * evaluations for f = 0), out[4f + 3] algorithmic bytes, both counted by the
  * kernels themselves from their actual dimensions.       */
-int hm_kernel_stats(hm_handle h, double out[20]);
+int hm_kernel_stats(hm_handle h, double out[24]);
 
 /* ---- dense fp64 check path (n <= 16384) --------------------------------- */
 /* Exact Eq. (1) on the GPU with dense Matern assembly, dense blocked

@@ -61,6 +61,7 @@ def _load():
         "hm_timings": ([P, P], C.c_int),
         "hm_profile": ([P, I32], C.c_int),
         "hm_kernel_stats": ([P, P], C.c_int),
+        "hm_set_exec_mode": ([P, I32], C.c_int),
         "hm_dense_loglik": ([P, I32, I64, Theta, P, I32, I32, I32, P, P], C.c_int),
         "hm_matern_block": ([P, I64, P, I64, Theta, I32, P], C.c_int),
     }
@@ -75,7 +76,7 @@ lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
             "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_matvec", "hm_stats", "hm_timings", "hm_profile",
-            "hm_kernel_stats",
+            "hm_kernel_stats", "hm_set_exec_mode",
             "hm_dense_loglik", "hm_matern_block")
 
 
@@ -253,10 +254,14 @@ class HMatrix:
     def profile(self, enable: bool):
         check(lib.hm_profile(self._h, 1 if enable else 0))
 
-    KERNEL_FAMILIES = ("k_dense_gen", "k_aca", "k_trunc", "k_vm", "k_aux")
+    KERNEL_FAMILIES = ("k_dense_gen", "k_aca", "k_trunc", "k_vm", "k_aux", "k_exec")
+
+    def set_exec_mode(self, mode: int):
+        """1 = persistent dependency-driven executor (default), 0 = one launch per wave."""
+        check(lib.hm_set_exec_mode(self._h, int(mode)))
 
     def kernel_stats(self) -> dict:
-        s = np.zeros(20)
+        s = np.zeros(24)
         check(lib.hm_kernel_stats(self._h, s.ctypes.data_as(C.c_void_p)))
         return {k: dict(launches=s[4 * i], ms=s[4 * i + 1], flops=s[4 * i + 2], bytes=s[4 * i + 3])
                 for i, k in enumerate(self.KERNEL_FAMILIES)}

@@ -191,6 +191,8 @@ int hm_plan_dump(hm_tree t, int32_t kmax, const char* path, double summary[8]) {
                 put(ph->tp.data(), (int64_t)ph->tp.size(), sizeof(TPiece));
                 put(ph->v_wave_begin.data(), (int64_t)ph->v_wave_begin.size(), 4);
                 put(ph->t_wave_begin.data(), (int64_t)ph->t_wave_begin.size(), 4);
+                put(ph->xt.data(), (int64_t)ph->xt.size(), sizeof(XTask));
+                put(ph->xdeps.data(), (int64_t)ph->xdeps.size(), 4);
             }
             std::fclose(f);
         }

@@ -6,9 +6,10 @@
 
 namespace hm {
 
-__device__ __forceinline__ int dim_eval(const Dim& d, const int* __restrict__ ranks) {
+// ranks are produced by other CTAs of the persistent executor: read through L2 (ld.cg)
+__device__ __forceinline__ int dim_eval(const Dim& d, const int* ranks) {
     if (d.slot < 0) return d.stat;
-    int v = ranks[d.slot] - d.off;
+    int v = __ldcg(ranks + d.slot) - d.off;
     return v < 0 ? 0 : (v > d.stat ? d.stat : v);
 }
 

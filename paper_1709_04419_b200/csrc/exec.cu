@@ -1,0 +1,86 @@
+// Persistent dependency-driven executor of a planned phase (H-Cholesky, solve,
+// sampler, recompression): one CTA per SM claims tasks in the planner's
+// topological order (global atomic counter), waits until every predecessor has
+// published completion (done[p] == epoch, acquire), runs the task -- a tile-VM
+// program (vm.cuh) or a low-rank truncation (trunc.cuh) -- and publishes its own
+// completion (release).  Claiming in topological order with all CTAs resident
+// makes the wait deadlock-free: the lowest unfinished claimed task always has
+// all its predecessors finished.  This replaces one launch (and one grid-wide
+// barrier) per wave by fine-grained edges, so independent tasks of different
+// waves overlap.
+#include <cuda_runtime.h>
+
+#include "dev_util.cuh"
+#include "hm_kernels.h"
+#include "hm_tasks.h"
+#include "tile.cuh"
+#include "trunc.cuh"
+#include "vm.cuh"
+
+namespace hm {
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(TTHREADS, 1)
+    k_exec(const XTask* __restrict__ xt, int nx, const int32_t* __restrict__ deps, const VTask* __restrict__ vt,
+           const VIns* __restrict__ ins, const TTask* __restrict__ tt, const TPiece* __restrict__ tp, double* pool,
+           int* ranks, int* flags, double* ctr, double eps, int* done, int* counter, int epoch) {
+    extern __shared__ double sm[];
+    __shared__ int s_task;
+    for (;;) {
+        if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+        __syncthreads();
+        const int i = s_task;
+        __syncthreads();
+        if (i >= nx) return;
+        const XTask x = xt[i];
+        if (threadIdx.x < 32) {
+            for (int d = threadIdx.x; d < x.dep_count; d += 32) {
+                const int* f = done + deps[x.dep_begin + d];
+                while (ld_acquire_gpu(f) != epoch) __nanosleep(40);
+            }
+            __syncwarp();
+            if (threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+        if (x.kind == 0) vm_run(vt[x.idx], ins, pool, ranks, flags, ctr, sm);
+        else trunc_run(tt[x.idx], tp, pool, ranks, flags, eps, ctr);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(done + i, epoch);
+        }
+    }
+}
+
+int exec_grid() {
+    static int grid = 0;
+    if (grid) return grid;
+    HM_CUDA_TRY(cudaFuncSetAttribute(k_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, NTILE * TSZ * 8));
+    int dev = 0, sms = 0, occ = 0;
+    HM_CUDA_TRY(cudaGetDevice(&dev));
+    HM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exec, TTHREADS, NTILE * TSZ * 8));
+    if (occ < 1) occ = 1;
+    grid = sms * occ;
+    return grid;
+}
+
+void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
+                 const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
+                 int* counter, int epoch, cudaStream_t st) {
+    if (nx <= 0) return;
+    const int grid = exec_grid();
+    HM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    k_exec<<<grid, TTHREADS, NTILE * TSZ * 8, st>>>(xt, nx, deps, vt, ins, tt, tp, pool, ranks, flags, ctr, eps, done,
+                                                   counter, epoch);
+}
+
+}  // namespace hm

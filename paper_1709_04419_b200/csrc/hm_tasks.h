@@ -80,6 +80,16 @@ inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot
            2 * L * L + 2 * L + 64;
 }
 
+// ---- dependency-driven execution (persistent executor, exec.cu) --------
+// All tasks of a phase in a topological order (sorted by wave); each lists the
+// positions of the tasks it must wait for (all smaller than its own).
+struct XTask {
+    int32_t kind;       // 0 = tile-VM program (vt[idx]), 1 = truncation (tt[idx])
+    int32_t idx;
+    int32_t dep_begin;  // into the phase's dependency array
+    int32_t dep_count;
+};
+
 // ---- assembly ------------------------------------------------------------
 struct DenseGenTask {         // D[i + j m] = C(|x_{r0+i} - x_{c0+j}|), i < m, j < q
     int64_t off;

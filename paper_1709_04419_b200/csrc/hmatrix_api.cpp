@@ -23,10 +23,10 @@
 
 namespace hm {
 
-enum KFamily { KF_DGEN = 0, KF_ACA = 1, KF_TRUNC = 2, KF_VM = 3, KF_AUX = 4, KF_N = 5 };
+enum KFamily { KF_DGEN = 0, KF_ACA = 1, KF_TRUNC = 2, KF_VM = 3, KF_AUX = 4, KF_EXEC = 5, KF_N = 6 };
 
 struct DPhase {
-    DevBuf ins, vt, tt, tp;
+    DevBuf ins, vt, tt, tp, xt, xd;
     const Phase* ph = nullptr;
 };
 
@@ -44,10 +44,14 @@ struct hm_handle_s {
     hm_theta theta{};
     MaternParams mp{};
     DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca, ctr;
+    // persistent executor state: completion flags (== epoch when done) and claim counter
+    DevBuf done, counter;
+    int epoch = 0;
+    int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
     // profiling: per kernel family (KF_*) launch counts (always) and, when
     // enabled, a CUDA event pair around every launch on the handle's stream
     bool profiling = false;
-    int64_t launches[KF_N] = {0, 0, 0, 0, 0};
+    int64_t launches[KF_N] = {0, 0, 0, 0, 0, 0};
     std::vector<cudaEvent_t> evpool;
     std::vector<std::pair<int, int>> evlog;   // (family, index of first event of the pair)
     DPhase rec, chol, solve, lmul;
@@ -78,6 +82,8 @@ void upload_phase(DPhase& d, const Phase& p, cudaStream_t st) {
     upload(d.vt, p.vt, st);
     upload(d.tt, p.tt, st);
     upload(d.tp, p.tp, st);
+    upload(d.xt, p.xt, st);
+    upload(d.xd, p.xdeps, st);
     d.ph = &p;
 }
 
@@ -110,6 +116,15 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
     int* ranks = h->ranks.as<int>();
     int* flags = h->flags.as<int>();
     double* ctr = h->ctr.as<double>();
+    if (h->exec_mode == 1) {
+        Launch L(h, KF_EXEC);
+        ++h->epoch;
+        launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
+                    d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
+                    h->counter.as<int>(), h->epoch, h->stream);
+        HM_CUDA_TRY(cudaGetLastError());
+        return;
+    }
     for (int w = 0; w < p.nwaves; ++w) {
         const int v0 = p.v_wave_begin[w], v1 = p.v_wave_begin[w + 1];
         const int t0 = p.t_wave_begin[w], t1 = p.t_wave_begin[w + 1];
@@ -274,6 +289,14 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         HM_CUDA_TRY(cudaMemsetAsync(h->ranks.p, 0, sizeof(int) * (h->P.n_slots + 1), h->stream));
         h->flags.alloc(sizeof(int) * 4);
         h->ctr.alloc(sizeof(double) * CTR_N);
+        {
+            size_t mx = 1;
+            for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) mx = std::max(mx, ph->xt.size());
+            h->done.alloc(sizeof(int) * mx);
+            HM_CUDA_TRY(cudaMemsetAsync(h->done.p, 0, sizeof(int) * mx, h->stream));
+            h->counter.alloc(sizeof(int) * 4);
+            exec_grid();
+        }
         HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
         h->out.alloc(sizeof(double) * 3 * h->P.zw);
         upload(h->dgen, h->P.dgen, h->stream);
@@ -467,12 +490,19 @@ int hm_profile(hm_handle h, int32_t enable) {
     }
 }
 
-int hm_kernel_stats(hm_handle h, double out[20]) {
+int hm_set_exec_mode(hm_handle h, int32_t mode) {
+    if (!h) return set_error(HM_ERR_ARG, "null handle");
+    if (mode != 0 && mode != 1) return set_error(HM_ERR_ARG, "mode must be 0 (waves) or 1 (persistent)");
+    h->exec_mode = mode;
+    return HM_OK;
+}
+
+int hm_kernel_stats(hm_handle h, double out[24]) {
     try {
         if (!h || !out) throw ApiError(HM_ERR_ARG, "null pointer");
         DeviceGuard dg(h->device);
         HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
-        double ms[KF_N] = {0, 0, 0, 0, 0};
+        double ms[KF_N] = {0, 0, 0, 0, 0, 0};
         for (auto& e : h->evlog) {
             float t = 0;
             HM_CUDA_TRY(cudaEventElapsedTime(&t, h->evpool[e.second], h->evpool[e.second + 1]));
@@ -480,13 +510,16 @@ int hm_kernel_stats(hm_handle h, double out[20]) {
         }
         double c[CTR_N];
         HM_CUDA_TRY(cudaMemcpy(c, h->ctr.p, sizeof(double) * CTR_N, cudaMemcpyDeviceToHost));
-        const int cmap[KF_N] = {CTR_DGEN, CTR_ACA, CTR_TRUNC, CTR_VM, -1};
+        const int cmap[KF_N] = {CTR_DGEN, CTR_ACA, CTR_TRUNC, CTR_VM, -1, -1};
         for (int f = 0; f < KF_N; ++f) {
             out[4 * f + 0] = (double)h->launches[f];
             out[4 * f + 1] = ms[f];
             out[4 * f + 2] = cmap[f] >= 0 ? c[cmap[f]] : 0.0;
             out[4 * f + 3] = cmap[f] >= 0 ? c[cmap[f] + 1] : 0.0;
         }
+        // the persistent executor runs the truncation and tile-VM tasks: its work is theirs
+        out[4 * KF_EXEC + 2] = c[CTR_TRUNC] + c[CTR_VM];
+        out[4 * KF_EXEC + 3] = c[CTR_TRUNC + 1] + c[CTR_VM + 1];
         return HM_OK;
     } catch (...) {
         return translate_exception();

@@ -67,13 +67,19 @@ struct Builder {
     int64_t bump = 0;
     int32_t nres = 0;
     std::vector<int32_t> lw_wave, rd_wave;
+    std::vector<int32_t> lw_task;                   // last writer task (creation id) per resource
+    std::vector<std::vector<int32_t>> rd_tasks;     // readers since the last write
     std::vector<Pend> pend;
+    struct XRaw { int32_t wave, kind, local; std::vector<int32_t> deps; };
+    std::vector<XRaw> xraw;
+    // truncation workspace ring: chunk-aligned bump allocation with wrap-around;
+    // every chunk is a resource, so reuse of a region orders after its last user
+    int64_t ring_chunk = 0, ring_nchunks = 0, ring_ptr = 0;
+    int32_t ring_res0 = -1;
     // current phase state
     Phase* ph = nullptr;
     std::vector<std::pair<int32_t, VTask>> vraw;   // (wave, task)
     std::vector<std::pair<int32_t, TTask>> traw;
-    std::vector<int64_t> ws_arena;                 // per-wave workspace usage (doubles)
-    int64_t ws_max_total = 0;
     int64_t n_tasks = 0;
 
     Builder(const Tree& t, Plan& p) : T(t), P(p) {}
@@ -91,11 +97,29 @@ struct Builder {
         nres += n;
         lw_wave.resize(nres, -1);
         rd_wave.resize(nres, -1);
+        lw_task.resize(nres, -1);
+        rd_tasks.resize(nres);
         return b;
     }
 
     // ---- dependency tracking ------------------------------------------
-    int32_t wave_of(const std::vector<int32_t>& reads, const std::vector<int32_t>& writes) {
+    int32_t wave_of(const std::vector<int32_t>& reads, const std::vector<int32_t>& writes,
+                    std::vector<int32_t>& deps) {
+        const int32_t me = (int32_t)xraw.size();
+        deps.clear();
+        for (int32_t r : reads)
+            if (lw_task[r] >= 0) deps.push_back(lw_task[r]);
+        for (int32_t r : writes) {
+            if (lw_task[r] >= 0) deps.push_back(lw_task[r]);
+            for (int32_t x : rd_tasks[r]) deps.push_back(x);
+        }
+        std::sort(deps.begin(), deps.end());
+        deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+        for (int32_t r : reads) rd_tasks[r].push_back(me);
+        for (int32_t r : writes) {
+            lw_task[r] = me;
+            rd_tasks[r].clear();
+        }
         int32_t w = 0;
         for (int32_t r : reads)
             if (lw_wave[r] >= 0) w = std::max(w, lw_wave[r] + 1);
@@ -117,11 +141,13 @@ struct Builder {
         pg.reads.erase(std::unique(pg.reads.begin(), pg.reads.end()), pg.reads.end());
         std::sort(pg.writes.begin(), pg.writes.end());
         pg.writes.erase(std::unique(pg.writes.begin(), pg.writes.end()), pg.writes.end());
-        int32_t w = wave_of(pg.reads, pg.writes);
+        std::vector<int32_t> deps;
+        int32_t w = wave_of(pg.reads, pg.writes, deps);
         VTask t;
         t.ins_begin = (int32_t)ph->ins.size();
         t.ins_count = (int32_t)pg.ins.size();
         ph->ins.insert(ph->ins.end(), pg.ins.begin(), pg.ins.end());
+        xraw.push_back({w, 0, (int32_t)vraw.size(), std::move(deps)});
         vraw.push_back({w, t});
         ++n_tasks;
     }
@@ -540,7 +566,20 @@ struct Builder {
         const BStore& s = P.bs[b];
         std::sort(reads.begin(), reads.end());
         reads.erase(std::unique(reads.begin(), reads.end()), reads.end());
-        int32_t w = wave_of(reads, writes);
+        int32_t kt0 = 0, wmax0 = 0;
+        for (auto& p : pcs) {
+            kt0 += p.w.stat;
+            wmax0 = std::max(wmax0, p.w.stat);
+        }
+        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, wmax0);
+        const int64_t nch = (wsz + ring_chunk - 1) / ring_chunk;
+        if (nch > ring_nchunks) throw std::logic_error("truncation workspace larger than the ring");
+        if (ring_ptr + nch > ring_nchunks) ring_ptr = 0;
+        const int64_t ws_off = P.ring_off + ring_ptr * ring_chunk;
+        for (int64_t c = 0; c < nch; ++c) writes.push_back(ring_res0 + (int32_t)(ring_ptr + c));
+        ring_ptr += nch;
+        std::vector<int32_t> deps;
+        int32_t w = wave_of(reads, writes, deps);
         TTask t{};
         t.u_out = s.u_off; t.v_out = s.v_off;
         t.m = s.m; t.q = s.p; t.cap = s.cap; t.rslot = s.rslot;
@@ -553,11 +592,10 @@ struct Builder {
         }
         t.kmax_tot = kt;
         t.wmax = wmax;
-        t.ws_size = trunc_ws_size(s.m, s.p, s.cap, kt, wmax);
-        if ((int)ws_arena.size() <= w) ws_arena.resize(w + 1, 0);
-        t.ws = ws_arena[w];           // relative; rebased after planning
-        ws_arena[w] += (t.ws_size + 31) & ~int64_t(31);
+        t.ws_size = wsz;
+        t.ws = ws_off;
         ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
+        xraw.push_back({w, 1, (int32_t)traw.size(), std::move(deps)});
         traw.push_back({w, t});
         ++n_tasks;
     }
@@ -613,16 +651,26 @@ struct Builder {
         ph = &p;
         vraw.clear();
         traw.clear();
-        ws_arena.clear();
+        xraw.clear();
+        ring_ptr = 0;
         std::fill(lw_wave.begin(), lw_wave.end(), -1);
         std::fill(rd_wave.begin(), rd_wave.end(), -1);
+        std::fill(lw_task.begin(), lw_task.end(), -1);
+        for (auto& v : rd_tasks) v.clear();
     }
     void end_phase() {
         int32_t nw = 0;
-        for (auto& v : vraw) nw = std::max(nw, v.first + 1);
-        for (auto& v : traw) nw = std::max(nw, v.first + 1);
-        std::stable_sort(vraw.begin(), vraw.end(), [](auto& a, auto& b) { return a.first < b.first; });
-        std::stable_sort(traw.begin(), traw.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        for (auto& v : xraw) nw = std::max(nw, v.wave + 1);
+        // stable order by wave of the VM / truncation lists (local -> sorted position)
+        auto sorted_pos = [](const auto& raw) {
+            std::vector<int32_t> idx(raw.size()), pos(raw.size());
+            for (size_t i = 0; i < raw.size(); ++i) idx[i] = (int32_t)i;
+            std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return raw[a].first < raw[b].first; });
+            for (size_t i = 0; i < idx.size(); ++i) pos[idx[i]] = (int32_t)i;
+            return std::make_pair(idx, pos);
+        };
+        auto [vidx, vpos] = sorted_pos(vraw);
+        auto [tidx, tpos] = sorted_pos(traw);
         ph->nwaves = nw;
         ph->v_wave_begin.assign(nw + 1, 0);
         ph->t_wave_begin.assign(nw + 1, 0);
@@ -632,25 +680,37 @@ struct Builder {
             size_t k = 0;
             for (int32_t w = 0; w < nw; ++w) {
                 ph->v_wave_begin[w] = (int32_t)k;
-                while (k < vraw.size() && vraw[k].first == w) ph->vt.push_back(vraw[k++].second);
+                while (k < vidx.size() && vraw[vidx[k]].first == w) ph->vt.push_back(vraw[vidx[k++]].second);
             }
             ph->v_wave_begin[nw] = (int32_t)k;
         }
-        // workspace: arenas are reused across waves (tasks of one wave run concurrently)
-        int64_t ws_need = 0;
-        for (auto x : ws_arena) ws_need = std::max(ws_need, x);
-        const int64_t ws_base = alloc(ws_need);
         {
             size_t k = 0;
             for (int32_t w = 0; w < nw; ++w) {
                 ph->t_wave_begin[w] = (int32_t)k;
-                while (k < traw.size() && traw[k].first == w) {
-                    TTask t = traw[k++].second;
-                    t.ws += ws_base;
-                    ph->tt.push_back(t);
-                }
+                while (k < tidx.size() && traw[tidx[k]].first == w) ph->tt.push_back(traw[tidx[k++]].second);
             }
             ph->t_wave_begin[nw] = (int32_t)k;
+        }
+        // unified topological list for the persistent executor
+        std::vector<int32_t> xidx(xraw.size()), xpos(xraw.size());
+        for (size_t i = 0; i < xraw.size(); ++i) xidx[i] = (int32_t)i;
+        std::stable_sort(xidx.begin(), xidx.end(), [&](int32_t a, int32_t b) { return xraw[a].wave < xraw[b].wave; });
+        for (size_t i = 0; i < xidx.size(); ++i) xpos[xidx[i]] = (int32_t)i;
+        ph->xt.clear();
+        ph->xdeps.clear();
+        for (size_t i = 0; i < xidx.size(); ++i) {
+            const XRaw& r = xraw[xidx[i]];
+            XTask x;
+            x.kind = r.kind;
+            x.idx = r.kind == 0 ? vpos[r.local] : tpos[r.local];
+            x.dep_begin = (int32_t)ph->xdeps.size();
+            for (int32_t d : r.deps) {
+                if (xpos[d] >= (int32_t)i) throw std::logic_error("planner: dependency not in topological order");
+                ph->xdeps.push_back(xpos[d]);
+            }
+            x.dep_count = (int32_t)ph->xdeps.size() - x.dep_begin;
+            ph->xt.push_back(x);
         }
         ph = nullptr;
     }
@@ -740,6 +800,22 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     P.z_off = bld.alloc((int64_t)T.n * P.zw);
     const int32_t z_res0 = bld.new_res(P.n_leaves);
     P.pool_blocks = bld.bump;
+    // truncation workspace ring: >= 4x the largest single workspace, >= 1 GiB
+    {
+        int64_t maxs = 0;
+        for (int32_t b = 0; b < nb; ++b) {
+            const BStore& s = P.bs[b];
+            if (s.kind != ST_LR) continue;
+            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K, s.cap));
+            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, std::max(s.cap, kmax)));
+        }
+        bld.ring_chunk = int64_t(1) << 16;   // 512 KiB
+        const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 27, 64 * maxs));
+        bld.ring_nchunks = (want + bld.ring_chunk - 1) / bld.ring_chunk;
+        P.ring_size = bld.ring_nchunks * bld.ring_chunk;
+        P.ring_off = bld.alloc(P.ring_size);
+        bld.ring_res0 = bld.new_res((int32_t)bld.ring_nchunks);
+    }
     // assembly tasks
     for (int32_t b = 0; b < nb; ++b) {
         const Block& bk = T.blocks[b];

@@ -44,6 +44,8 @@ struct Phase {                   // one executable phase (levelled task lists)
     std::vector<TTask> tt;       // sorted by wave
     std::vector<TPiece> tp;
     std::vector<int32_t> v_wave_begin, t_wave_begin;  // size nwaves + 1
+    std::vector<XTask> xt;       // every task, topological (wave) order
+    std::vector<int32_t> xdeps;  // predecessor positions in xt
     int32_t nwaves = 0;
     int64_t n_launches() const;
 };
@@ -65,6 +67,7 @@ struct Plan {
     int64_t z_off = 0;                 // solve RHS buffer: n x ZW (col-major, ld n)
     int32_t zw = 64;
     int64_t bytes_C = 0;               // bytes of block storage at capacity
+    int64_t ring_off = 0, ring_size = 0;  // truncation workspace ring (doubles)
     // assembly
     std::vector<DenseGenTask> dgen;
     std::vector<AcaTask> aca;

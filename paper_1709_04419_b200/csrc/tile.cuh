@@ -96,10 +96,12 @@ __device__ __forceinline__ void tile_zero(double* T) {
 }
 
 // Load rows x cols (col-major, leading dim ld) from global into a zero-padded tile.
-__device__ __forceinline__ void tile_load(double* T, const double* __restrict__ G, int64_t ld, int rows, int cols) {
+// (ld.global.cg: the source may have been written by another CTA of the same
+// persistent kernel, so the read-only / L1 paths are not used)
+__device__ __forceinline__ void tile_load(double* T, const double* G, int64_t ld, int rows, int cols) {
     for (int idx = threadIdx.x; idx < TD * TD; idx += blockDim.x) {
         const int r = idx & (TD - 1), c = idx >> 6;
-        T[c * TLD + r] = (r < rows && c < cols) ? G[(int64_t)c * ld + r] : 0.0;
+        T[c * TLD + r] = (r < rows && c < cols) ? __ldcg(G + (int64_t)c * ld + r) : 0.0;
     }
 }
 

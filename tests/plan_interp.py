@@ -49,9 +49,16 @@ def _read(path):
     return out
 
 
+XTASK = np.dtype([("kind", "<i4"), ("idx", "<i4"), ("dep_begin", "<i4"), ("dep_count", "<i4")])
+
+
 class Phase:
     def __init__(self, secs):
-        (ni, si, bi), (nv, sv, bv), (nt, st, bt), (np_, sp, bp), (nw1, _, bw1), (nw2, _, bw2) = secs
+        (ni, si, bi), (nv, sv, bv), (nt, st, bt), (np_, sp, bp), (nw1, _, bw1), (nw2, _, bw2), (nx, sx, bx), \
+            (nd, _, bd) = secs
+        assert sx == XTASK.itemsize
+        self.xt = np.frombuffer(bx, XTASK, nx)
+        self.xdeps = np.frombuffer(bd, "<i4", nd)
         assert si == VINS.itemsize and sv == VTASK.itemsize and st == TTASK.itemsize and sp == TPIECE.itemsize
         self.ins = np.frombuffer(bi, VINS, ni)
         self.vt = np.frombuffer(bv, VTASK, nv)
@@ -70,12 +77,18 @@ class Plan:
         assert secs[1][1] == DGEN.itemsize and secs[2][1] == ACA.itemsize
         self.dgen = np.frombuffer(secs[1][2], DGEN, secs[1][0])
         self.aca = np.frombuffer(secs[2][2], ACA, secs[2][0])
-        self.phases = [Phase(secs[3 + 6 * i: 9 + 6 * i]) for i in range(4)]
+        self.phases = [Phase(secs[3 + 8 * i: 11 + 8 * i]) for i in range(4)]
         self.recompress, self.chol, self.solve, self.lmul = self.phases
 
 
 class Interp:
-    def __init__(self, plan: Plan, eps: float, seed: int = 0):
+    """mode "waves": tasks of each wave in random order, waves in sequence (the
+    launch-per-wave executor).  mode "dag": a random topological order that
+    respects only the explicit dependency lists xt/xdeps (what the persistent
+    executor k_exec enforces) -- a missing edge shows up as a wrong answer."""
+
+    def __init__(self, plan: Plan, eps: float, seed: int = 0, mode: str = "waves"):
+        self.mode = mode
         self.P = plan
         self.eps = eps
         self.pool = np.zeros(plan.pool_total)
@@ -200,6 +213,8 @@ class Interp:
         self.ranks[t["rslot"]] = r
 
     def run(self, ph):
+        if self.mode == "dag":
+            return self.run_dag(ph)
         for w in range(ph.nwaves):
             jobs = [("v", i) for i in range(ph.vwb[w], ph.vwb[w + 1])] + \
                    [("t", i) for i in range(ph.twb[w], ph.twb[w + 1])]
@@ -208,6 +223,34 @@ class Interp:
                     self.vm(ph, ph.vt[i])
                 else:
                     self.trunc(ph, ph.tt[i])
+
+    def run_dag(self, ph):
+        n = len(ph.xt)
+        succ = [[] for _ in range(n)]
+        indeg = np.zeros(n, dtype=np.int64)
+        for i, x in enumerate(ph.xt):
+            for d in ph.xdeps[x["dep_begin"]: x["dep_begin"] + x["dep_count"]]:
+                assert d < i, "dependency must precede the task in xt order"
+                succ[int(d)].append(i)
+                indeg[i] += 1
+        ready = [i for i in range(n) if indeg[i] == 0]
+        done = 0
+        while ready:
+            j = int(self.rng.integers(len(ready)))
+            i = ready[j]
+            ready[j] = ready[-1]
+            ready.pop()
+            x = ph.xt[i]
+            if x["kind"] == 0:
+                self.vm(ph, ph.vt[x["idx"]])
+            else:
+                self.trunc(ph, ph.tt[x["idx"]])
+            done += 1
+            for s2 in succ[i]:
+                indeg[s2] -= 1
+                if indeg[s2] == 0:
+                    ready.append(s2)
+        assert done == n
 
     # ---------------------------------------------------------------- likelihood
     def loglik(self, Z_tree):

@@ -98,3 +98,23 @@ def test_errors(hm):
     H = hm.HMatrix(pts, (1.0, 0.1, 0.5), eps=1e-6, leaf=16)
     with pytest.raises(hm.HMError):
         H.loglik(np.zeros(100))           # before cholesky
+
+
+@pytest.mark.parametrize("n,leaf", [(2000, 32), (3000, 16)])
+def test_exec_modes_identical(hm, n, leaf):
+    """Persistent dependency-driven executor (default) vs one launch per wave:
+    the same tasks with the same inputs -> bit-identical likelihoods."""
+    pts = uniform_iid(n, seed=21)
+    theta = (1.0, 0.0864, 0.5)
+    Z = standard_normal(n, 2, seed=22)
+    outs = []
+    for mode in (0, 1):
+        H = hm.HMatrix(pts, theta, eps=1e-7, leaf=leaf, eta=2.0)
+        H.set_exec_mode(mode)
+        H.assemble(theta)
+        H.cholesky()
+        outs.append(H.loglik(Z))
+        H.close()
+    assert np.array_equal(outs[0], outs[1])
+    oll, _, _ = od.loglik(pts, Z, theta)
+    np.testing.assert_allclose(outs[1][:, 0], oll, rtol=1e-5)

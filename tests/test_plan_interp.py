@@ -10,14 +10,14 @@ from synthetic import uniform_iid, standard_normal, perturbed_mesh
 from plan_interp import Plan, Interp
 
 
-def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2):
+def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2, mode="waves"):
     from paper_1709_04419_b200 import Tree
     t = Tree(pts, leaf, eta)
     path = str(tmp_path / "plan.bin")
     t.plan_dump(path, kmax)
     P = Plan(path)
     perm = t.perm()
-    I = Interp(P, eps, seed=seed)
+    I = Interp(P, eps, seed=seed, mode=mode)
     I.assemble(pts[perm], theta)
     I.run(P.chol)
     assert I.fail == 0
@@ -32,6 +32,15 @@ def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2):
 def test_planner_matches_dense_oracle(tmp_path, n, leaf, eta, eps, seed):
     pts = uniform_iid(n, seed)
     ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), leaf, eta, eps, seed=seed)
+    np.testing.assert_allclose(ll, oll, rtol=1e-8)
+    assert abs(ld - old) <= 1e-6 * abs(old) + 1e-6
+
+
+@pytest.mark.parametrize("n,leaf,eta,seed", [(600, 16, 2.0, 10), (1024, 8, 3.0, 11)])
+def test_planner_dependency_edges(tmp_path, n, leaf, eta, seed):
+    """Persistent-executor order: any topological order of xt/xdeps gives the result."""
+    pts = uniform_iid(n, seed)
+    ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), leaf, eta, 1e-10, seed=seed, mode="dag")
     np.testing.assert_allclose(ll, oll, rtol=1e-8)
     assert abs(ld - old) <= 1e-6 * abs(old) + 1e-6
 
