@@ -1,0 +1,3 @@
+python paper_1709_04419_b200/build.py > /dev/null
+timeout 600 python tools/hm_probe2.py > gpurun_out/probe2.txt 2>&1; cat gpurun_out/probe2.txt
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt; tail -15 gpurun_out/pytest_gpu.txt
