@@ -164,6 +164,14 @@ int hm_profile(hm_handle h, int32_t enable);
  * 0 = one launch per wave and task type (k_trunc, k_vm).  Same arithmetic.     */
 int hm_set_exec_mode(hm_handle h, int32_t mode);
 
+/* Diagnostics: hm_trace(h, 1, NULL) makes the persistent executor record, for
+ * every task of each subsequent phase launch, (claim, dependencies-satisfied,
+ * end) %globaltimer nanoseconds and (sm id | kind << 16 | CTA << 32), 4 uint64
+ * per task in the phase's topological task order; hm_trace(h, e, path) first
+ * writes the record of the LAST executor launch to the binary file `path`
+ * (if path != NULL), then sets tracing to e.                                */
+int hm_trace(hm_handle h, int32_t enable, const char* path);
+
 /* Per kernel family f = 0..5 (dense Matern block generation, ACA, low-rank
  * truncation, tile VM, auxiliary gather/finish, persistent executor -- whose
  * flops/bytes are those of the truncation + VM tasks it ran): out[4f + 0] launches since

@@ -10,6 +10,8 @@
 // waves overlap.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "dev_util.cuh"
 #include "hm_kernels.h"
 #include "hm_tasks.h"
@@ -18,6 +20,8 @@
 #include "vm.cuh"
 
 namespace hm {
+
+constexpr int EXEC_SMEM = (NTILE * TSZ * 8 > TR_SMEM) ? NTILE * TSZ * 8 : TR_SMEM;
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;
@@ -28,10 +32,11 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(TTHREADS, 1)
+__global__ void __launch_bounds__(TTHREADS, 2)
     k_exec(const XTask* __restrict__ xt, int nx, const int32_t* __restrict__ deps, const VTask* __restrict__ vt,
            const VIns* __restrict__ ins, const TTask* __restrict__ tt, const TPiece* __restrict__ tp, double* pool,
-           int* ranks, int* flags, double* ctr, double eps, int* done, int* counter, int epoch) {
+           int* ranks, int* flags, double* ctr, double eps, int* done, int* counter, int epoch,
+           unsigned long long* trace) {
     extern __shared__ double sm[];
     __shared__ int s_task;
     for (;;) {
@@ -41,6 +46,8 @@ __global__ void __launch_bounds__(TTHREADS, 1)
         __syncthreads();
         if (i >= nx) return;
         const XTask x = xt[i];
+        unsigned long long t_claim = 0, t_ready = 0;
+        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_claim));
         if (threadIdx.x < 32) {
             for (int d = threadIdx.x; d < x.dep_count; d += 32) {
                 const int* f = done + deps[x.dep_begin + d];
@@ -50,12 +57,23 @@ __global__ void __launch_bounds__(TTHREADS, 1)
             if (threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
         __syncthreads();
+        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
         if (x.kind == 0) vm_run(vt[x.idx], ins, pool, ranks, flags, ctr, sm);
-        else trunc_run(tt[x.idx], tp, pool, ranks, flags, eps, ctr);
+        else trunc_run(tt[x.idx], tp, pool, ranks, flags, eps, ctr, sm);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
             st_release_gpu(done + i, epoch);
+            if (trace) {   // per task: claim, ready (deps satisfied), end [ns], sm id | kind << 16
+                unsigned long long t_end;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                unsigned int smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                trace[4 * (size_t)i + 0] = t_claim;
+                trace[4 * (size_t)i + 1] = t_ready;
+                trace[4 * (size_t)i + 2] = t_end;
+                trace[4 * (size_t)i + 3] = smid | ((unsigned long long)x.kind << 16) | ((unsigned long long)blockIdx.x << 32);
+            }
         }
     }
 }
@@ -63,24 +81,28 @@ __global__ void __launch_bounds__(TTHREADS, 1)
 int exec_grid() {
     static int grid = 0;
     if (grid) return grid;
-    HM_CUDA_TRY(cudaFuncSetAttribute(k_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, NTILE * TSZ * 8));
+    HM_CUDA_TRY(cudaFuncSetAttribute(k_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM));
     int dev = 0, sms = 0, occ = 0;
     HM_CUDA_TRY(cudaGetDevice(&dev));
     HM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exec, TTHREADS, NTILE * TSZ * 8));
+    HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exec, TTHREADS, EXEC_SMEM));
     if (occ < 1) occ = 1;
     grid = sms * occ;
+    if (const char* g = std::getenv("HM_EXEC_GRID")) {   // debug: fewer persistent CTAs
+        const int v = std::atoi(g);
+        if (v > 0 && v < grid) grid = v;
+    }
     return grid;
 }
 
 void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
-                 int* counter, int epoch, cudaStream_t st) {
+                 int* counter, int epoch, unsigned long long* trace, cudaStream_t st) {
     if (nx <= 0) return;
     const int grid = exec_grid();
     HM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_exec<<<grid, TTHREADS, NTILE * TSZ * 8, st>>>(xt, nx, deps, vt, ins, tt, tp, pool, ranks, flags, ctr, eps, done,
-                                                   counter, epoch);
+    k_exec<<<grid, TTHREADS, EXEC_SMEM, st>>>(xt, nx, deps, vt, ins, tt, tp, pool, ranks, flags, ctr, eps, done,
+                                              counter, epoch, trace);
 }
 
 }  // namespace hm

@@ -18,7 +18,7 @@ enum VmOp : uint8_t {
     VM_TRMM_LN = 7,  // tile[t0] <- tile[t1] tile[t0]
     VM_ZERO = 8,     // tile[t0] <- 0 with dims (rows x cols)
 };
-constexpr int NTILE = 5;
+constexpr int NTILE = 3;   // target + two operands (TRSM/TRMM reuse tile 1 for L)
 
 // Dimension spec: actual = (slot < 0) ? stat : clamp(ranks[slot] - off, 0, stat)
 struct Dim {

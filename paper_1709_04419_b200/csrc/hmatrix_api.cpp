@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -48,6 +49,9 @@ struct hm_handle_s {
     DevBuf done, counter;
     int epoch = 0;
     int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
+    DevBuf trace;        // per-task timestamps of the last executor launch (hm_trace)
+    bool tracing = false;
+    int64_t trace_n = 0;
     // profiling: per kernel family (KF_*) launch counts (always) and, when
     // enabled, a CUDA event pair around every launch on the handle's stream
     bool profiling = false;
@@ -121,7 +125,9 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         ++h->epoch;
         launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
                     d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
-                    h->counter.as<int>(), h->epoch, h->stream);
+                    h->counter.as<int>(), h->epoch,
+                    h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->stream);
+        if (h->tracing) h->trace_n = (int64_t)p.xt.size();
         HM_CUDA_TRY(cudaGetLastError());
         return;
     }
@@ -484,6 +490,31 @@ int hm_profile(hm_handle h, int32_t enable) {
         for (auto& x : h->launches) x = 0;
         HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
         HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_trace(hm_handle h, int32_t enable, const char* path) {
+    try {
+        if (!h) throw ApiError(HM_ERR_ARG, "null handle");
+        DeviceGuard dg(h->device);
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        if (path && h->trace_n > 0) {
+            std::vector<unsigned long long> buf(4 * (size_t)h->trace_n);
+            HM_CUDA_TRY(cudaMemcpy(buf.data(), h->trace.p, buf.size() * 8, cudaMemcpyDeviceToHost));
+            FILE* f = std::fopen(path, "wb");
+            if (!f) throw ApiError(HM_ERR_ARG, std::string("cannot open ") + path);
+            std::fwrite(buf.data(), 8, buf.size(), f);
+            std::fclose(f);
+        }
+        if (enable) {
+            size_t mx = 1;
+            for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) mx = std::max(mx, ph->xt.size());
+            h->trace.alloc(32 * mx);
+        }
+        h->tracing = enable != 0;
         return HM_OK;
     } catch (...) {
         return translate_exception();

@@ -636,8 +636,8 @@ struct Builder {
             Prog pg;
             ld_dense(pg, 0, b);
             apply_dense_pending(pg, b);
-            ld_dense(pg, 3, P.diag_of[s]);
-            op2(pg, VM_TRSM_RLT, 0, 3);
+            ld_dense(pg, 1, P.diag_of[s]);
+            op2(pg, VM_TRSM_RLT, 0, 1);
             st_dense(pg, 0, b);
             emit_vm(pg);
         } else {

@@ -162,9 +162,10 @@ static __device__ __noinline__ void jacobi_svd(double* X, int rows, int n, doubl
 
 // ---------------------------------------------------------------- exact path
 static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restrict__ pieces, double* __restrict__ pool,
-                            int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr) {
+                            int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
+                            double* dsm) {
     __shared__ double scratch[32];
-    __shared__ int order[ORDER_MAX];
+    int* order = (int*)dsm;                        // ORDER_MAX ints (dynamic shared memory)
     __shared__ int s_flag;
     __shared__ int s_rank;
     const int m = t.m, q = t.q;
@@ -296,7 +297,8 @@ __device__ __forceinline__ void warp_sum_arr(double* acc) {
 }
 
 static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restrict__ pieces, double* __restrict__ pool,
-                           int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr) {
+                           int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
+                           double* dsm) {
     const int m = t.m, q = t.q, cap = t.cap;
     const int L = cap + TR_RB;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -310,13 +312,13 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     double* Z = S + (int64_t)L * L;                // L x L
     double* tau = Z + (int64_t)L * L;              // L
     double* sig = tau + L;                         // L
-    __shared__ double Tp[TR_WMAX_SM * TR_RB];      // per-piece T_p = V_p^T Omega (w x RB)
-    __shared__ double Cs[(TR_LMAX) * TR_RB];       // Q^T Y  (ell x RB)
+    double* Tp = dsm;                              // per-piece T_p = V_p^T Omega (TR_WMAX_SM x RB)
+    double* Cs = Tp + TR_WMAX_SM * TR_RB;          // Q^T Y  (TR_LMAX x RB)
     __shared__ double scratch[32];
     __shared__ int s_added, s_rank, s_flag;
     __shared__ double s_ratio[TR_RB];
     __shared__ int s_alive[TR_RB];
-    __shared__ int order[ORDER_MAX];
+    int* order = (int*)(Cs + TR_LMAX * TR_RB);     // ORDER_MAX ints
     const uint64_t seed = (uint64_t)t.u_out * 0x632BE59BD9B4E019ull;
     int ell = 0;
     double sest = 0.0;
@@ -442,9 +444,38 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             if (step == 0) maxn = best;
             const int na = s_added;
             if (!(best > thr) || ell + na >= L) break;
+            // re-orthogonalise the pivot against the whole basis (old + new), twice:
+            // its residual can be ~eps below its original norm, so the rounding of
+            // the earlier projections must be removed before normalising
+            double* yp = Yn + (int64_t)jp * m;
+            const int nb = ell + na;
+            for (int pass = 0; pass < 2 && nb > 0; ++pass) {
+                for (int l = warp; l < nb; l += nw) {
+                    const double* ql = Qm + (int64_t)l * m;
+                    double d = 0.0;
+                    for (int i = lane; i < m; i += 32) d += ql[i] * yp[i];
+                    d = warp_sum(d);
+                    if (lane == 0) Cs[l] = d;
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                    double a = 0.0;
+                    for (int l = 0; l < nb; ++l) a += Qm[i + (int64_t)l * m] * Cs[l];
+                    yp[i] -= a;
+                }
+                __syncthreads();
+            }
+            double nn = 0.0;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) nn += yp[i] * yp[i];
+            const double nrm = sqrt(block_sum(nn, scratch));
+            if (!(nrm > thr)) {                    // only rounding left: drop the probe
+                if (threadIdx.x == 0) s_alive[jp] = 0;
+                __syncthreads();
+                continue;
+            }
             double* qn = Qm + (int64_t)(ell + na) * m;
-            const double inv = 1.0 / best;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) qn[i] = Yn[i + (int64_t)jp * m] * inv;
+            const double inv = 1.0 / nrm;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) qn[i] = yp[i] * inv;
             __syncthreads();
             if (threadIdx.x == 0) { s_alive[jp] = 0; s_added = na + 1; }
             for (int j = warp; j < TR_RB; j += nw) {
@@ -585,12 +616,15 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     }
 }
 
+// dynamic shared memory (bytes) the truncation needs
+constexpr int TR_SMEM = (TR_WMAX_SM * TR_RB + TR_LMAX * TR_RB) * 8 + ORDER_MAX * 4;
+
 __device__ __forceinline__ void trunc_run(const TTask& t, const TPiece* __restrict__ pieces, double* pool, int* ranks,
-                                          int* flags, double eps, double* ctr) {
+                                          int* flags, double eps, double* ctr, double* dsm) {
     int K = 0;
     for (int p = 0; p < t.piece_count; ++p) K += dim_eval(pieces[t.piece_begin + p].w, ranks);
-    if (t.kmax_tot <= TR_EXACT_K) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr);
-    else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr);
+    if (t.kmax_tot <= TR_EXACT_K) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
+    else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
 }
 
 }  // namespace hm

@@ -275,3 +275,76 @@ class Interp:
         self.pool[self.P.z_off:self.P.z_off + n * zw] = buf.ravel(order="F")
         self.run(self.P.lmul)
         return self.pool[self.P.z_off:self.P.z_off + n * zw].reshape(zw, n).T[:, :k].copy()
+
+
+class InterpRand(Interp):
+    """Interp whose wide truncations follow the device's randomized range finder
+    (trunc.cuh, trunc_rand) step by step: rounds of RB Gaussian probes, twice
+    projected against Q, column-pivoted MGS with threshold eps * sigma_est / 8,
+    then W = M^T Q, QR, SVD.  Used to check that algorithm on the CPU."""
+    RB = 16
+    EXACT_K = 160
+
+    def trunc(self, ph, t):
+        if int(t["kmax_tot"]) <= self.EXACT_K:
+            return super().trunc(ph, t)
+        m, q, cap = int(t["m"]), int(t["q"]), int(t["cap"])
+        As, Bs = [], []
+        for pc in ph.tp[t["piece_begin"]: t["piece_begin"] + t["piece_count"]]:
+            w = self.dim(pc["w"])
+            A = np.zeros((m, w)); B = np.zeros((q, w))
+            A[pc["u_row0"]:pc["u_row0"] + pc["u_rows"]] = pc["alpha"] * self.gload(int(pc["u_off"]), int(pc["u_ld"]),
+                                                                                  int(pc["u_rows"]), w)
+            B[pc["v_row0"]:pc["v_row0"] + pc["v_rows"]] = self.gload(int(pc["v_off"]), int(pc["v_ld"]),
+                                                                     int(pc["v_rows"]), w)
+            As.append(A); Bs.append(B)
+        A = np.concatenate(As, axis=1); B = np.concatenate(Bs, axis=1)
+        L = cap + self.RB
+        Q = np.zeros((m, 0))
+        sest = 0.0
+        while True:
+            Om = self.rng.standard_normal((q, self.RB))
+            Y = A @ (B.T @ Om)
+            sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0) / np.linalg.norm(Om, axis=0))))
+            thr = self.eps * sest / 8
+            for _ in range(2):
+                Y = Y - Q @ (Q.T @ Y)
+            alive = list(range(self.RB))
+            added = []
+            maxn = None
+            while alive:
+                nr = [np.linalg.norm(Y[:, j]) for j in alive]
+                jb = int(np.argmax(nr))
+                best = nr[jb]
+                if maxn is None:
+                    maxn = best
+                if not best > thr or Q.shape[1] + len(added) >= L:
+                    break
+                jp = alive.pop(jb)
+                Qc = np.concatenate([Q] + ([np.stack(added, 1)] if added else []), axis=1)
+                y = Y[:, jp].copy()
+                for _ in range(2):                      # re-orthogonalise against the whole basis
+                    y -= Qc @ (Qc.T @ y)
+                nrm = np.linalg.norm(y)
+                if not nrm > thr:
+                    continue
+                qn = y / nrm
+                added.append(qn)
+                for j in alive:
+                    for _ in range(2):
+                        Y[:, j] -= (qn @ Y[:, j]) * qn
+            if added:
+                Q = np.concatenate([Q, np.stack(added, 1)], axis=1)
+            if maxn <= thr or not added or Q.shape[1] >= L or Q.shape[1] >= m or Q.shape[1] >= q:
+                break
+        if Q.shape[1] == 0:
+            self.ranks[t["rslot"]] = 0
+            return
+        W = B @ (A.T @ Q)                       # M^T Q
+        Qw, R = np.linalg.qr(W)
+        X, S, Zt = np.linalg.svd(R.T)           # R^T = X S Z^T
+        r = int(np.sum((S > self.eps * S[0]) & (S > 0)))
+        r = min(r, cap)
+        self.gstore(int(t["u_out"]), m, (Q @ X[:, :r]) * S[:r])
+        self.gstore(int(t["v_out"]), q, Qw @ Zt[:r].T)
+        self.ranks[t["rslot"]] = r

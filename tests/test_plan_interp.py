@@ -7,17 +7,17 @@ import pytest
 
 from oracle import dense as od
 from synthetic import uniform_iid, standard_normal, perturbed_mesh
-from plan_interp import Plan, Interp
+from plan_interp import Plan, Interp, InterpRand
 
 
-def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2, mode="waves"):
+def _run(tmp_path, pts, theta, leaf, eta, eps, kmax=64, seed=0, k=2, mode="waves", cls=Interp):
     from paper_1709_04419_b200 import Tree
     t = Tree(pts, leaf, eta)
     path = str(tmp_path / "plan.bin")
     t.plan_dump(path, kmax)
     P = Plan(path)
     perm = t.perm()
-    I = Interp(P, eps, seed=seed, mode=mode)
+    I = cls(P, eps, seed=seed, mode=mode)
     I.assemble(pts[perm], theta)
     I.run(P.chol)
     assert I.fail == 0
@@ -43,6 +43,18 @@ def test_planner_dependency_edges(tmp_path, n, leaf, eta, seed):
     ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), leaf, eta, 1e-10, seed=seed, mode="dag")
     np.testing.assert_allclose(ll, oll, rtol=1e-8)
     assert abs(ld - old) <= 1e-6 * abs(old) + 1e-6
+
+
+@pytest.mark.parametrize("eps,tol", [(1e-10, 1e-9), (1e-7, 1e-5)])
+def test_randomized_truncation_algorithm(tmp_path, eps, tol):
+    """The device's randomized range-finder truncation (trunc.cuh), replayed with
+    numpy on the wide Cholesky truncations, keeps the likelihood at the accuracy
+    eps allows (n = 2000, leaf 32: stacked widths reach ~1700 columns).  At
+    eps = 1e-10 this needs the full re-orthogonalisation of each new basis vector."""
+    pts = uniform_iid(2000, 11)
+    ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), 32, 2.0, eps, kmax=160, seed=0, k=1,
+                                         cls=InterpRand)
+    np.testing.assert_allclose(ll, oll, rtol=tol)
 
 
 def test_planner_general_nu_mesh(tmp_path):

@@ -1,0 +1,75 @@
+"""Analyse a persistent-executor trace (hm_trace) of one phase against its plan.
+
+usage (on the GPU box, see tools/hm_trace_probe.py): writes a text summary:
+makespan, per-kind busy time, utilisation, dependency-wait time, the critical
+path through the dependency DAG with measured task durations, and the longest
+tasks.
+"""
+from __future__ import annotations
+
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/repo/tests")
+from plan_interp import Plan  # noqa: E402
+
+
+def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 296, top: int = 15) -> str:
+    P = Plan(plan_path)
+    ph = getattr(P, phase)
+    tr = np.fromfile(trace_path, dtype=np.uint64).reshape(-1, 4)
+    n = len(ph.xt)
+    assert tr.shape[0] == n, (tr.shape, n)
+    t0 = tr[:, 0].min()
+    claim = (tr[:, 0] - t0).astype(np.float64) * 1e-3   # us
+    ready = (tr[:, 1] - t0).astype(np.float64) * 1e-3
+    end = (tr[:, 2] - t0).astype(np.float64) * 1e-3
+    kind = ph.xt["kind"]
+    dur = end - ready
+    wait = ready - claim
+    mk = end.max()
+    lines = [f"phase={phase} tasks={n} makespan={mk / 1e3:.3f} ms grid={grid}"]
+    for k, nm in ((0, "vm"), (1, "trunc")):
+        sel = kind == k
+        lines.append(f"  {nm:6s} n={sel.sum():8d} busy={dur[sel].sum() / 1e3:10.3f} ms  mean={dur[sel].mean() if sel.any() else 0:8.2f} us"
+                     f"  max={dur[sel].max() if sel.any() else 0:9.1f} us  dep-wait={wait[sel].sum() / 1e3:9.3f} ms")
+    lines.append(f"  utilisation (busy / (makespan * grid)) = {dur.sum() / (mk * grid):.3f}")
+    # critical path with measured durations
+    cp = np.zeros(n)
+    arg = np.full(n, -1)
+    for i in range(n):
+        x = ph.xt[i]
+        d = ph.xdeps[x["dep_begin"]: x["dep_begin"] + x["dep_count"]]
+        if d.size:
+            j = d[np.argmax(cp[d])]
+            cp[i] = cp[j] + dur[i]
+            arg[i] = j
+        else:
+            cp[i] = dur[i]
+    i = int(np.argmax(cp))
+    path = []
+    while i >= 0:
+        path.append(i)
+        i = int(arg[i])
+    path.reverse()
+    pk = kind[path]
+    lines.append(f"  critical path: {cp.max() / 1e3:.3f} ms over {len(path)} tasks "
+                 f"(vm {int((pk == 0).sum())}: {dur[path][pk == 0].sum() / 1e3:.3f} ms, "
+                 f"trunc {int((pk == 1).sum())}: {dur[path][pk == 1].sum() / 1e3:.3f} ms)")
+    order = np.argsort(-dur)[:top]
+    lines.append("  longest tasks:")
+    for i in order:
+        x = ph.xt[i]
+        if x["kind"] == 1:
+            t = ph.tt[x["idx"]]
+            desc = f"trunc m={t['m']} q={t['q']} cap={t['cap']} Kstat={t['kmax_tot']} pieces={t['piece_count']}"
+        else:
+            v = ph.vt[x["idx"]]
+            desc = f"vm ins={v['ins_count']}"
+        lines.append(f"    #{i:7d} {dur[i]:10.1f} us  on_cp={i in set(path)}  {desc}")
+    return "\n".join(lines)
+
+
+if __name__ == "__main__":
+    print(analyse(*sys.argv[1:3], phase=sys.argv[3] if len(sys.argv) > 3 else "chol"))
