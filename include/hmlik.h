@@ -172,6 +172,12 @@ int hm_set_exec_mode(hm_handle h, int32_t mode);
  * (if path != NULL), then sets tracing to e.                                */
 int hm_trace(hm_handle h, int32_t enable, const char* path);
 
+/* Diagnostics: checksums of the current block storage (C~ or L~): out[0] sum
+ * of |entries| of dense blocks, out[1] a position-weighted sum of them, out[2]
+ * sum of |entries| of the first rank(b) columns of every U_b, V_b, out[3] sum
+ * of the ranks.  Copies the block storage to the host (slow; tests only).     */
+int hm_checksum(hm_handle h, double out[4]);
+
 /* Per kernel family f = 0..5 (dense Matern block generation, ACA, low-rank
  * truncation, tile VM, auxiliary gather/finish, persistent executor -- whose
  * flops/bytes are those of the truncation + VM tasks it ran): out[4f + 0] launches since

@@ -63,6 +63,7 @@ def _load():
         "hm_kernel_stats": ([P, P], C.c_int),
         "hm_set_exec_mode": ([P, I32], C.c_int),
         "hm_trace": ([P, I32, C.c_char_p], C.c_int),
+        "hm_checksum": ([P, P], C.c_int),
         "hm_dense_loglik": ([P, I32, I64, Theta, P, I32, I32, I32, P, P], C.c_int),
         "hm_matern_block": ([P, I64, P, I64, Theta, I32, P], C.c_int),
     }
@@ -77,7 +78,7 @@ lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
             "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_matvec", "hm_stats", "hm_timings", "hm_profile",
-            "hm_kernel_stats", "hm_set_exec_mode", "hm_trace",
+            "hm_kernel_stats", "hm_set_exec_mode", "hm_trace", "hm_checksum",
             "hm_dense_loglik", "hm_matern_block")
 
 
@@ -264,6 +265,11 @@ class HMatrix:
     def trace(self, enable: bool, path: str | None = None):
         """Per-task executor timestamps (diagnostics); see hm_trace in include/hmlik.h."""
         check(lib.hm_trace(self._h, 1 if enable else 0, path.encode() if path else None))
+
+    def checksum(self) -> np.ndarray:
+        s = np.zeros(4)
+        check(lib.hm_checksum(self._h, s.ctypes.data_as(C.c_void_p)))
+        return s
 
     def kernel_stats(self) -> dict:
         s = np.zeros(24)

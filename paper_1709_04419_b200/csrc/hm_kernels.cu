@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__
             continue;
         }
         const double delta = V[jstar + (int64_t)k * q];
+        __syncthreads();   // every thread has read the pivot before its owner rescales it in place
         for (int j = threadIdx.x; j < q; j += blockDim.x) V[j + (int64_t)k * q] /= delta;
         __syncthreads();
         // ---- residual column jstar -> U[:, k]

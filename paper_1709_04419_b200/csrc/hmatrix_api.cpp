@@ -496,6 +496,37 @@ int hm_profile(hm_handle h, int32_t enable) {
     }
 }
 
+int hm_checksum(hm_handle h, double out[4]) {
+    try {
+        if (!h || !out) throw ApiError(HM_ERR_ARG, "null pointer");
+        DeviceGuard dg(h->device);
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        const Plan& P = h->P;
+        std::vector<double> pool((size_t)P.pool_blocks);
+        HM_CUDA_TRY(cudaMemcpy(pool.data(), h->pool.p, sizeof(double) * pool.size(), cudaMemcpyDeviceToHost));
+        max_rank(h);
+        double sd = 0, sl = 0, sr = 0, sw = 0;
+        for (size_t b = 0; b < P.bs.size(); ++b) {
+            const BStore& st = P.bs[b];
+            if (st.kind == ST_DENSE) {
+                for (int64_t i = 0; i < (int64_t)st.m * st.p; ++i) {
+                    sd += std::fabs(pool[st.d_off + i]);
+                    sw += pool[st.d_off + i] * (double)((i % 97) + 1);
+                }
+            } else if (st.kind == ST_LR) {
+                const int r = h->h_ranks[st.rslot];
+                sr += r;
+                for (int64_t i = 0; i < (int64_t)st.m * r; ++i) sl += std::fabs(pool[st.u_off + i]);
+                for (int64_t i = 0; i < (int64_t)st.p * r; ++i) sl += std::fabs(pool[st.v_off + i]);
+            }
+        }
+        out[0] = sd; out[1] = sw; out[2] = sl; out[3] = sr;
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
 int hm_trace(hm_handle h, int32_t enable, const char* path) {
     try {
         if (!h) throw ApiError(HM_ERR_ARG, "null handle");

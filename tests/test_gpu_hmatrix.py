@@ -118,3 +118,22 @@ def test_exec_modes_identical(hm, n, leaf):
     assert np.array_equal(outs[0], outs[1])
     oll, _, _ = od.loglik(pts, Z, theta)
     np.testing.assert_allclose(outs[1][:, 0], oll, rtol=1e-5)
+
+
+def test_repeat_evaluations_bit_identical(hm):
+    """Assembly (ACA + recompression), H-Cholesky and solve are deterministic:
+    repeated evaluations on the same inputs agree bit for bit (this caught a
+    read-before-rescale race on the ACA pivot)."""
+    pts = uniform_iid(16384, 1)
+    theta = (1.0, 0.0334, 0.5)
+    Z = standard_normal(16384, 1, 3)
+    H = hm.HMatrix(pts, theta, eps=1e-8, leaf=32, eta=2.0)
+    sums, outs = [], []
+    for _ in range(3):
+        H.assemble(theta)
+        sums.append(H.checksum())
+        H.cholesky()
+        outs.append(H.loglik(Z))
+    for s, o in zip(sums[1:], outs[1:]):
+        assert np.array_equal(s, sums[0])
+        assert np.array_equal(o, outs[0])
