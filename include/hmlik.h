@@ -167,7 +167,9 @@ int hm_set_exec_mode(hm_handle h, int32_t mode);
 /* Diagnostics: hm_trace(h, 1, NULL) makes the persistent executor record, for
  * every task of each subsequent phase launch, (claim, dependencies-satisfied,
  * end) %globaltimer nanoseconds and (sm id | kind << 16 | CTA << 32), 4 uint64
- * per task in the phase's topological task order; hm_trace(h, e, path) first
+ * per task in the phase's topological task order, followed by 64 uint64 per
+ * task (randomized truncations: start and each stage boundary; else 0);
+ * hm_trace(h, e, path) first
  * writes the record of the LAST executor launch to the binary file `path`
  * (if path != NULL), then sets tracing to e.                                */
 int hm_trace(hm_handle h, int32_t enable, const char* path);

@@ -6,6 +6,15 @@
 
 namespace hm {
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ranks are produced by other CTAs of the persistent executor: read through L2 (ld.cg)
 __device__ __forceinline__ int dim_eval(const Dim& d, const int* ranks) {
     if (d.slot < 0) return d.stat;

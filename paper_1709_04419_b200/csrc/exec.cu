@@ -23,20 +23,12 @@ namespace hm {
 
 constexpr int EXEC_SMEM = (NTILE * TSZ * 8 > TR_SMEM) ? NTILE * TSZ * 8 : TR_SMEM;
 
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __global__ void __launch_bounds__(TTHREADS, 2)
     k_exec(const XTask* __restrict__ xt, int nx, const int32_t* __restrict__ deps, const VTask* __restrict__ vt,
            const VIns* __restrict__ ins, const TTask* __restrict__ tt, const TPiece* __restrict__ tp, double* pool,
            int* ranks, int* flags, double* ctr, double eps, int* done, int* counter, int epoch,
-           unsigned long long* trace) {
+           unsigned long long* trace, int* bars) {
     extern __shared__ double sm[];
     __shared__ int s_task;
     for (;;) {
@@ -59,7 +51,11 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         __syncthreads();
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
         if (x.kind == 0) vm_run(vt[x.idx], ins, pool, ranks, flags, ctr, sm);
-        else trunc_run(tt[x.idx], tp, pool, ranks, flags, eps, ctr, sm);
+        else {
+            const TTask t = tt[x.idx];
+            trunc_run(t, tp, pool, ranks, flags, eps, ctr, sm, x.sub, x.nsub, bars + t.bar,
+                      trace ? trace + 4 * (size_t)nx + 64 * (size_t)i : nullptr);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -97,12 +93,13 @@ int exec_grid() {
 
 void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
-                 int* counter, int epoch, unsigned long long* trace, cudaStream_t st) {
+                 int* counter, int epoch, unsigned long long* trace, int* bars, int nbars, cudaStream_t st) {
     if (nx <= 0) return;
     const int grid = exec_grid();
     HM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    if (nbars > 0) HM_CUDA_TRY(cudaMemsetAsync(bars, 0, sizeof(int) * nbars, st));
     k_exec<<<grid, TTHREADS, EXEC_SMEM, st>>>(xt, nx, deps, vt, ins, tt, tp, pool, ranks, flags, ctr, eps, done,
-                                              counter, epoch, trace);
+                                              counter, epoch, trace, bars);
 }
 
 }  // namespace hm

@@ -20,7 +20,7 @@ void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* 
 int exec_grid();
 void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
-                 int* counter, int epoch, unsigned long long* trace, cudaStream_t st);
+                 int* counter, int epoch, unsigned long long* trace, int* bars, int nbars, cudaStream_t st);
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st);
 void launch_scatter(const double* Zt, const int64_t* perm, int64_t n, int kz, double* Z, cudaStream_t st);
 void launch_finish(const double* logd, int nleaves, const double* Zt, int64_t n, int kz, double* out,

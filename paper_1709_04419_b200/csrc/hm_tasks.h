@@ -4,6 +4,12 @@
 #pragma once
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define HM_HD __host__ __device__
+#else
+#define HM_HD
+#endif
+
 namespace hm {
 
 // ---- tile VM -------------------------------------------------------------
@@ -63,21 +69,59 @@ struct TTask {
     int32_t piece_begin, piece_count;
     int32_t kmax_tot;         // sum of static piece widths
     int32_t wmax;             // largest static piece width
+    int32_t nsub;             // CTAs cooperating on this truncation (persistent executor)
+    int32_t bar;              // index of its group barrier counter
 };
 
-// k_trunc algorithm selection and workspace (trunc.cu; planner sizes the workspace)
+// k_trunc algorithm selection and workspace (trunc.cuh; planner sizes the workspace)
 constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs
 constexpr int TR_RB = 16;         // probes per round of the randomized range finder
-constexpr int TR_WMAX_SM = 64;    // piece columns staged per shared-memory chunk
 constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
+constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
+constexpr int TR_TCH = 128;       // stacked columns staged per shared-memory chunk
+constexpr int TR_PMAX = 1023;     // pieces per truncation
+constexpr int64_t TR_COOP_WORK = int64_t(1) << 18;   // (m + q) * static K per cooperating CTA
+constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
+
+struct TruncWs {                  // randomized-path workspace (doubles unless noted)
+    double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp;
+    int64_t total;
+};
+HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t cap, int32_t Ks,
+                                     int32_t wmax) {
+    (void)wmax;
+    const int64_t L = (int64_t)cap + TR_RB;
+    const int64_t nch = (m + TR_RCH - 1) / TR_RCH + (q + TR_RCH - 1) / TR_RCH;
+    TruncWs w;
+    int64_t o = 0;
+    const int64_t sz[21] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_RB, (int64_t)m * Ks, (int64_t)q * Ks,
+                            (int64_t)TR_RB * Ks, (int64_t)m * TR_RB, nch * TR_RB, (int64_t)m * L, L * TR_RB,
+                            L * (int64_t)Ks, (int64_t)q * L, (int64_t)q * L, L * L, L * L, L * L, L * L, L, L,
+                            (int64_t)TR_COOP_MAX * L * TR_RB, (int64_t)TR_COOP_MAX * L * TR_RB,
+                            (int64_t)TR_COOP_MAX * TR_RB * TR_RB};
+    double* ptr[21];
+    for (int i = 0; i < 21; ++i) {
+        ptr[i] = base + o;
+        o += (sz[i] + 7) & ~int64_t(7);
+    }
+    w.ctl = ptr[0]; w.Om = ptr[1]; w.Ast = ptr[2]; w.Bst = ptr[3]; w.Tt = ptr[4]; w.Y = ptr[5];
+    w.npart = ptr[6]; w.Q = ptr[7]; w.Cb = ptr[8]; w.Pt = ptr[9]; w.Wm = ptr[10]; w.Wc = ptr[11];
+    w.S = ptr[12]; w.Z = ptr[13]; w.Xo = ptr[14]; w.G = ptr[15]; w.tau = ptr[16]; w.sig = ptr[17];
+    w.Cp = ptr[18]; w.Cf = ptr[19]; w.Gp = ptr[20];
+    w.total = o + 64;
+    return w;
+}
 inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot, int32_t wmax) {
     if (kmax_tot <= TR_EXACT_K) {
         const int64_t K = kmax_tot;
         return ((int64_t)m + q + 2 * K + 8) * K + 64;
     }
-    const int64_t L = (int64_t)cap + TR_RB;
-    return (int64_t)q * TR_RB + (int64_t)m * L + (int64_t)m * TR_RB + (int64_t)q * L + (int64_t)wmax * L +
-           2 * L * L + 2 * L + 64;
+    return trunc_ws_layout(nullptr, m, q, cap, kmax_tot, wmax).total;
+}
+inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
+    if (kmax_tot <= TR_EXACT_K) return 1;
+    const int64_t g = ((int64_t)(m + q) * kmax_tot) / TR_COOP_WORK;
+    return (int32_t)(g < 1 ? 1 : (g > TR_COOP_MAX ? TR_COOP_MAX : g));
 }
 
 // ---- dependency-driven execution (persistent executor, exec.cu) --------
@@ -88,6 +132,7 @@ struct XTask {
     int32_t idx;
     int32_t dep_begin;  // into the phase's dependency array
     int32_t dep_count;
+    int32_t sub, nsub;  // cooperative truncation: this CTA's index / group size (else 0 / 1)
 };
 
 // ---- assembly ------------------------------------------------------------

@@ -46,7 +46,7 @@ struct hm_handle_s {
     MaternParams mp{};
     DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca, ctr;
     // persistent executor state: completion flags (== epoch when done) and claim counter
-    DevBuf done, counter;
+    DevBuf done, counter, bars;
     int epoch = 0;
     int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
     DevBuf trace;        // per-task timestamps of the last executor launch (hm_trace)
@@ -123,10 +123,12 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
     if (h->exec_mode == 1) {
         Launch L(h, KF_EXEC);
         ++h->epoch;
+        if (h->tracing)
+            HM_CUDA_TRY(cudaMemsetAsync((char*)h->trace.p + 32 * p.xt.size(), 0, 8 * 64 * p.xt.size(), h->stream));
         launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
                     d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
                     h->counter.as<int>(), h->epoch,
-                    h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->stream);
+                    h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(), p.n_bars, h->stream);
         if (h->tracing) h->trace_n = (int64_t)p.xt.size();
         HM_CUDA_TRY(cudaGetLastError());
         return;
@@ -301,6 +303,9 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
             h->done.alloc(sizeof(int) * mx);
             HM_CUDA_TRY(cudaMemsetAsync(h->done.p, 0, sizeof(int) * mx, h->stream));
             h->counter.alloc(sizeof(int) * 4);
+            int nb = 1;
+            for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) nb = std::max(nb, ph->n_bars);
+            h->bars.alloc(sizeof(int) * nb);
             exec_grid();
         }
         HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
@@ -533,7 +538,7 @@ int hm_trace(hm_handle h, int32_t enable, const char* path) {
         DeviceGuard dg(h->device);
         HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
         if (path && h->trace_n > 0) {
-            std::vector<unsigned long long> buf(4 * (size_t)h->trace_n);
+            std::vector<unsigned long long> buf(68 * (size_t)h->trace_n);
             HM_CUDA_TRY(cudaMemcpy(buf.data(), h->trace.p, buf.size() * 8, cudaMemcpyDeviceToHost));
             FILE* f = std::fopen(path, "wb");
             if (!f) throw ApiError(HM_ERR_ARG, std::string("cannot open ") + path);
@@ -543,7 +548,7 @@ int hm_trace(hm_handle h, int32_t enable, const char* path) {
         if (enable) {
             size_t mx = 1;
             for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) mx = std::max(mx, ph->xt.size());
-            h->trace.alloc(32 * mx);
+            h->trace.alloc(8 * 68 * mx);   // 4 per task + 64 truncation stage stamps per task
         }
         h->tracing = enable != 0;
         return HM_OK;

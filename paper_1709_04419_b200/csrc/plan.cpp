@@ -75,7 +75,7 @@ struct Builder {
     // truncation workspace ring: chunk-aligned bump allocation with wrap-around;
     // every chunk is a resource, so reuse of a region orders after its last user
     int64_t ring_chunk = 0, ring_nchunks = 0, ring_ptr = 0;
-    int32_t ring_res0 = -1;
+    std::vector<int32_t> ring_res;                  // resource id of each chunk (the ring can grow)
     // current phase state
     Phase* ph = nullptr;
     std::vector<std::pair<int32_t, VTask>> vraw;   // (wave, task)
@@ -100,6 +100,11 @@ struct Builder {
         lw_task.resize(nres, -1);
         rd_tasks.resize(nres);
         return b;
+    }
+
+    void grow_ring(int64_t nchunks) {
+        while ((int64_t)ring_res.size() < nchunks) ring_res.push_back(new_res(1));
+        ring_nchunks = (int64_t)ring_res.size();
     }
 
     // ---- dependency tracking ------------------------------------------
@@ -550,7 +555,6 @@ struct Builder {
         Pend pd = std::move(pend[b]);
         pend[b] = Pend();
         if (!force && pd.prods.empty() && pd.pieces.empty()) return;
-        const BStore& s = P.bs[b];
         std::vector<TPiece> pcs;
         std::vector<int32_t> reads, writes;
         pcs.push_back(tpiece(thin_U(b), thin_V(b), 0, 0, 1.0, reads));
@@ -573,10 +577,10 @@ struct Builder {
         }
         const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, wmax0);
         const int64_t nch = (wsz + ring_chunk - 1) / ring_chunk;
-        if (nch > ring_nchunks) throw std::logic_error("truncation workspace larger than the ring");
+        if (4 * nch > ring_nchunks) grow_ring(4 * nch);   // keep >= 4 workspaces of this size in flight
         if (ring_ptr + nch > ring_nchunks) ring_ptr = 0;
-        const int64_t ws_off = P.ring_off + ring_ptr * ring_chunk;
-        for (int64_t c = 0; c < nch; ++c) writes.push_back(ring_res0 + (int32_t)(ring_ptr + c));
+        const int64_t ws_off = ring_ptr * ring_chunk;    // relative to the ring; rebased after planning
+        for (int64_t c = 0; c < nch; ++c) writes.push_back(ring_res[ring_ptr + c]);
         ring_ptr += nch;
         std::vector<int32_t> deps;
         int32_t w = wave_of(reads, writes, deps);
@@ -594,6 +598,9 @@ struct Builder {
         t.wmax = wmax;
         t.ws_size = wsz;
         t.ws = ws_off;
+        if ((int32_t)pcs.size() > TR_PMAX) throw std::logic_error("truncation with more than TR_PMAX pieces");
+        t.nsub = trunc_nsub(s.m, s.p, kt);
+        t.bar = t.nsub > 1 ? ph->n_bars++ : 0;
         ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
         xraw.push_back({w, 1, (int32_t)traw.size(), std::move(deps)});
         traw.push_back({w, t});
@@ -649,6 +656,7 @@ struct Builder {
     // ---- phase bookkeeping -------------------------------------------------
     void begin_phase(Phase& p) {
         ph = &p;
+        p.n_bars = 0;
         vraw.clear();
         traw.clear();
         xraw.clear();
@@ -697,20 +705,36 @@ struct Builder {
         for (size_t i = 0; i < xraw.size(); ++i) xidx[i] = (int32_t)i;
         std::stable_sort(xidx.begin(), xidx.end(), [&](int32_t a, int32_t b) { return xraw[a].wave < xraw[b].wave; });
         for (size_t i = 0; i < xidx.size(); ++i) xpos[xidx[i]] = (int32_t)i;
+        // a cooperative truncation occupies nsub consecutive entries (leader first);
+        // its successors wait on the leader, which publishes after the group's last barrier
+        std::vector<int32_t> xlead(xraw.size());
+        {
+            int32_t pos = 0;
+            for (size_t i = 0; i < xidx.size(); ++i) {
+                const XRaw& r = xraw[xidx[i]];
+                xlead[xidx[i]] = pos;
+                pos += (r.kind == 1) ? ph->tt[tpos[r.local]].nsub : 1;
+            }
+        }
         ph->xt.clear();
         ph->xdeps.clear();
         for (size_t i = 0; i < xidx.size(); ++i) {
             const XRaw& r = xraw[xidx[i]];
-            XTask x;
+            XTask x{};
             x.kind = r.kind;
             x.idx = r.kind == 0 ? vpos[r.local] : tpos[r.local];
             x.dep_begin = (int32_t)ph->xdeps.size();
+            const int32_t me = xlead[xidx[i]];
             for (int32_t d : r.deps) {
-                if (xpos[d] >= (int32_t)i) throw std::logic_error("planner: dependency not in topological order");
-                ph->xdeps.push_back(xpos[d]);
+                if (xlead[d] >= me) throw std::logic_error("planner: dependency not in topological order");
+                ph->xdeps.push_back(xlead[d]);
             }
             x.dep_count = (int32_t)ph->xdeps.size() - x.dep_begin;
-            ph->xt.push_back(x);
+            x.nsub = (r.kind == 1) ? ph->tt[x.idx].nsub : 1;
+            for (int32_t sb = 0; sb < x.nsub; ++sb) {
+                x.sub = sb;
+                ph->xt.push_back(x);
+            }
         }
         ph = nullptr;
     }
@@ -800,7 +824,8 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     P.z_off = bld.alloc((int64_t)T.n * P.zw);
     const int32_t z_res0 = bld.new_res(P.n_leaves);
     P.pool_blocks = bld.bump;
-    // truncation workspace ring: >= 4x the largest single workspace, >= 1 GiB
+    // truncation workspace ring: starts at >= 4x the largest recompression workspace
+    // (min 128 MiB) and grows to >= 4x the largest workspace the Cholesky emits
     {
         int64_t maxs = 0;
         for (int32_t b = 0; b < nb; ++b) {
@@ -810,11 +835,8 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
             maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, std::max(s.cap, kmax)));
         }
         bld.ring_chunk = int64_t(1) << 16;   // 512 KiB
-        const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 27, 64 * maxs));
-        bld.ring_nchunks = (want + bld.ring_chunk - 1) / bld.ring_chunk;
-        P.ring_size = bld.ring_nchunks * bld.ring_chunk;
-        P.ring_off = bld.alloc(P.ring_size);
-        bld.ring_res0 = bld.new_res((int32_t)bld.ring_nchunks);
+        const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 24, 64 * maxs));
+        bld.grow_ring((want + bld.ring_chunk - 1) / bld.ring_chunk);
     }
     // assembly tasks
     for (int32_t b = 0; b < nb; ++b) {
@@ -851,6 +873,11 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     bld.begin_phase(P.lmul);
     bld.lmul(0, Z);
     bld.end_phase();
+    // place the ring and rebase every truncation workspace offset onto it
+    P.ring_size = bld.ring_nchunks * bld.ring_chunk;
+    P.ring_off = bld.alloc(P.ring_size);
+    for (Phase* ph : {&P.recompress, &P.chol, &P.solve, &P.lmul})
+        for (TTask& t : ph->tt) t.ws += P.ring_off;
     P.pool_total = bld.bump;
 }
 

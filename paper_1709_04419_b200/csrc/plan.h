@@ -46,6 +46,7 @@ struct Phase {                   // one executable phase (levelled task lists)
     std::vector<int32_t> v_wave_begin, t_wave_begin;  // size nwaves + 1
     std::vector<XTask> xt;       // every task, topological (wave) order
     std::vector<int32_t> xdeps;  // predecessor positions in xt
+    int32_t n_bars = 0;          // group barriers of cooperative truncations
     int32_t nwaves = 0;
     int64_t n_launches() const;
 };

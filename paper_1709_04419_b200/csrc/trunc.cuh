@@ -34,11 +34,25 @@
 #include "dev_util.cuh"
 #include "hm_kernels.h"
 #include "hm_tasks.h"
+#include "gemm.cuh"
+#include "tile.cuh"
 
 namespace hm {
 
 constexpr int TR_THREADS = 256;
 constexpr int ORDER_MAX = 512;
+// Range-finder stopping rule.  For a Gaussian probe w, E ||R w||^2 = ||R||_F^2, so
+// the probe norms ||M w_j|| estimate ||M||_F and the projected-probe norms
+// ||(I - Q Q^T) M w_j|| estimate ||M - Q Q^T M||_F.  The basis is complete when
+// every projected probe of a round is <= TR_STOP * eps * max_j ||M w_j|| (first
+// round): relative accuracy ~eps in the Frobenius norm, hence also in the
+// spectral one, before the final SVD truncation at eps * sigma_1.  (A spectral
+// certificate would have to capture the flat tail of truncation noise the
+// accumulated Cholesky updates carry just below eps * sigma_1: ~4x the final
+// rank measured at n = 64k.)
+constexpr double TR_STOP = 1.0;
+// dynamic shared memory: [Cs (leader) | staging] then order, koff
+constexpr int TR_SMEM_A = 8 * GEMM_SMEM_DOUBLES;   // GEMM staging, then order / koff
 
 // Householder QR of A (m x K, ld m) in place; tau[K].  R in the upper triangle.
 static __device__ __noinline__ void house_qr(double* A, int m, int K, double* tau, double* scratch) {
@@ -296,335 +310,440 @@ __device__ __forceinline__ void warp_sum_arr(double* acc) {
     for (int j = 0; j < TR_RB; ++j) acc[j] = warp_sum(acc[j]);
 }
 
+
+// Barrier among the nsub CTAs of one cooperative truncation (persistent executor
+// only: the nsub sub-tasks are consecutive in the claim order, nsub <= grid).
+__device__ __forceinline__ void coop_sync(int* bar, int nsub, int& gen, unsigned long long* st = nullptr) {
+    if (st && threadIdx.x == 0 && gen < 62) {   // stage timestamps (diagnostics, hm_trace)
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        st[gen + 1] = now;
+    }
+    __syncthreads();
+    ++gen;
+    if (nsub > 1) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(bar, 1);
+            const int target = gen * nsub;
+            while (ld_acquire_gpu(bar) < target) __nanosleep(32);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+    }
+}
+
+// piece containing stacked column k (koff: prefix widths, np + 1 entries)
+__device__ __forceinline__ int piece_of(const int* koff, int np, int k) {
+    int lo = 0, hi = np - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (koff[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+
+
+// X[:, 0:nc] <- X - Q[:, 0:ell] (Q^T X) on this CTA's own row chunks; the ell x nc
+// product is reduced over the group through per-CTA partials (one barrier).
+__device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int L, double* X, int nc, int sub, int nsub,
+                                           int nchm, int* bar, int& gen, unsigned long long* stt, double* gsm) {
+    double* Cp = W.Cp + (int64_t)sub * L * TR_RB;
+    bool first = true;
+    for (int c = sub; c < nchm; c += nsub) {
+        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
+        gemm_short(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
+                   gsm);
+        first = false;
+    }
+    if (first)
+        for (int idx = threadIdx.x; idx < ell * nc; idx += blockDim.x) Cp[(idx % ell) + (int64_t)(idx / ell) * L] = 0.0;
+    coop_sync(bar, nsub, gen, stt);
+    double* Cf = W.Cf + (int64_t)sub * L * TR_RB;
+    for (int idx = threadIdx.x; idx < ell * nc; idx += blockDim.x) {
+        const int64_t e = (idx % ell) + (int64_t)(idx / ell) * L;
+        double a = 0.0;
+        for (int s2 = 0; s2 < nsub; ++s2) a += __ldcg(W.Cp + (int64_t)s2 * L * TR_RB + e);
+        Cf[e] = a;
+    }
+    __syncthreads();
+    for (int c = sub; c < nchm; c += nsub) {
+        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
+        gemm_narrow(rows, nc, ell, -1.0, gop(W.Q + r0, m, false), gop(Cf, L, false), 1.0, X + r0, m, 0, 1, gsm);
+    }
+    // (no barrier: the partials are re-written only after the next coop_sync, and X's
+    //  own rows are touched only by this CTA)
+}
+
+// Gs (shared, nc x nc, ld TR_RB) = X[:, 0:nc]^T X[:, 0:nc], reduced over the group
+__device__ __forceinline__ void gram_owned(const TruncWs& W, int m, const double* X, int nc, int sub, int nsub,
+                                           int nchm, int* bar, int& gen, unsigned long long* stt, double* gsm,
+                                           double* Gs) {
+    double* Gp = W.Gp + (int64_t)sub * TR_RB * TR_RB;
+    bool first = true;
+    for (int c = sub; c < nchm; c += nsub) {
+        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
+        gemm_short(nc, nc, rows, 1.0, gop(X + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Gp, TR_RB, 0, 1,
+                   gsm);
+        first = false;
+    }
+    if (first)
+        for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) Gp[(idx % nc) + (idx / nc) * TR_RB] = 0.0;
+    coop_sync(bar, nsub, gen, stt);
+    for (int idx = threadIdx.x; idx < TR_RB * TR_RB; idx += blockDim.x) {
+        const int i = idx % TR_RB, j = idx / TR_RB;
+        double a = 0.0;
+        if (i < nc && j < nc)
+            for (int s2 = 0; s2 < nsub; ++s2) a += __ldcg(W.Gp + (int64_t)s2 * TR_RB * TR_RB + i + j * TR_RB);
+        Gs[i * TR_RB + j] = a;                     // symmetric: row/col order immaterial
+    }
+    __syncthreads();
+}
+
+// Randomized adaptive truncation, executed by nsub CTAs (sub = this CTA's index;
+// sub 0 = leader).  The pieces are gathered once into contiguous stacks
+// U_stack (m x K) and V_stack (q x K); every heavy pass is then a pipelined DMMA
+// GEMM whose output tiles are spread over the group (gemm.cuh):
+//   R2  T^T = Omega^T V_stack              (16 x K)
+//   R3  Y   = U_stack T                    (m x 16)
+//   R4  block classical Gram-Schmidt, twice (BCGS2): Y -= Q (Q^T Y) twice,
+//       column-pivoted MGS of the block with the eps threshold (leader), the new
+//       columns re-projected against the old basis and re-normalised
+//   F1  P^T = Q^T U_stack                  (ell x K)
+//   F2  W   = V_stack P                    (q x ell)   (= M^T Q)
+//   F3  W = Q_W R (Householder), R^T = X' Z^T (one-sided Jacobi), rank (leader)
+//   F4  U = Q X'(:, order),  V = W X'(:, order) Sigma^-2  (= Q_W Z)
+// Work tiles are fixed, so the result does not depend on nsub.
 static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restrict__ pieces, double* __restrict__ pool,
-                           int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
-                           double* dsm) {
-    const int m = t.m, q = t.q, cap = t.cap;
+                                  int* __restrict__ ranks, int* __restrict__ flags, double eps,
+                                  double* __restrict__ ctr, double* dsm, int sub, int nsub, int* bar,
+                                  unsigned long long* stt) {
+    const int m = t.m, q = t.q, cap = t.cap, np = t.piece_count;
     const int L = cap + TR_RB;
+    const int Ks = t.kmax_tot;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double* ws = pool + t.ws;
-    double* Om = ws;                              // q x RB
-    double* Qm = Om + (int64_t)q * TR_RB;          // m x L
-    double* Yn = Qm + (int64_t)m * L;              // m x RB
-    double* Wm = Yn + (int64_t)m * TR_RB;          // q x L
-    double* Pp = Wm + (int64_t)q * L;              // wmax x L
-    double* S = Pp + (int64_t)t.wmax * L;          // L x L
-    double* Z = S + (int64_t)L * L;                // L x L
-    double* tau = Z + (int64_t)L * L;              // L
-    double* sig = tau + L;                         // L
-    double* Tp = dsm;                              // per-piece T_p = V_p^T Omega (TR_WMAX_SM x RB)
-    double* Cs = Tp + TR_WMAX_SM * TR_RB;          // Q^T Y  (TR_LMAX x RB)
+    const int nchm = (m + TR_RCH - 1) / TR_RCH, nchq = (q + TR_RCH - 1) / TR_RCH;
+    TruncWs W = trunc_ws_layout(pool + t.ws, m, q, cap, Ks, t.wmax);
+    int* ctl = (int*)W.ctl;                        // [0] done, [1] ell, [2] rank, [3] added, [8..] order
+    double* gsm = dsm;                             // GEMM staging
+    int* koff = (int*)((char*)dsm + TR_SMEM_A + ORDER_MAX * 4);   // TR_PMAX + 1 ints
+    int* order = (int*)((char*)dsm + TR_SMEM_A);   // ORDER_MAX ints (leader, F3)
     __shared__ double scratch[32];
     __shared__ int s_added, s_rank, s_flag;
     __shared__ double s_ratio[TR_RB];
-    __shared__ int s_alive[TR_RB];
-    int* order = (int*)(Cs + TR_LMAX * TR_RB);     // ORDER_MAX ints
+    __shared__ double Gs[TR_RB * TR_RB], Rs[TR_RB * TR_RB];
+    __shared__ int piv[TR_RB];
+    __shared__ int s_na;
+    __shared__ double s_maxn;
+    int gen = 0;
+    if (sub != 0) stt = nullptr;
+    if (stt && threadIdx.x == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        stt[0] = now;
+    }
+    if (np > TR_PMAX) {                            // planner guarantees np <= TR_PMAX
+        if (threadIdx.x == 0 && sub == 0) atomicOr(flags + 1, 4);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int p = 0; p < np; ++p) {
+            koff[p] = acc;
+            acc += dim_eval(pieces[t.piece_begin + p].w, ranks);
+        }
+        koff[np] = acc;
+    }
+    __syncthreads();
+    // gather the stacks A = [alpha_p pad(U_p)] (m x K) and B = [pad(V_p)] (q x K): every
+    // CTA copies whole 64-row pieces of its columns with many independent loads in flight
+    {
+        const int mrb = (m + 63) / 64, qrb = (q + 63) / 64;
+        const int64_t nitem = (int64_t)K * (mrb + qrb);
+        for (int64_t it = (int64_t)sub * 4 + (threadIdx.x >> 6); it < nitem; it += (int64_t)nsub * 4) {
+            const int k = (int)(it / (mrb + qrb)), rb = (int)(it % (mrb + qrb));
+            const int p = piece_of(koff, np, k);
+            const TPiece pc = pieces[t.piece_begin + p];
+            const int c = k - koff[p];
+            const int lrow = threadIdx.x & 63;
+            if (rb < mrb) {
+                const int i = rb * 64 + lrow;
+                if (i < m) {
+                    const int ii = i - pc.u_row0;
+                    W.Ast[i + (int64_t)k * m] =
+                        (ii >= 0 && ii < pc.u_rows) ? pc.alpha * __ldcg(pool + pc.u_off + (int64_t)c * pc.u_ld + ii) : 0.0;
+                }
+            } else {
+                const int i = (rb - mrb) * 64 + lrow;
+                if (i < q) {
+                    const int ii = i - pc.v_row0;
+                    W.Bst[i + (int64_t)k * q] =
+                        (ii >= 0 && ii < pc.v_rows) ? __ldcg(pool + pc.v_off + (int64_t)c * pc.v_ld + ii) : 0.0;
+                }
+            }
+        }
+    }
+    double Srows = 0.0;                            // sum over stacked columns of (u_rows + v_rows)
+    for (int p = 0; p < np; ++p)
+        Srows += (double)(koff[p + 1] - koff[p]) * (pieces[t.piece_begin + p].u_rows + pieces[t.piece_begin + p].v_rows);
     const uint64_t seed = (uint64_t)t.u_out * 0x632BE59BD9B4E019ull;
+    const GOp Ust = gop(W.Ast, m, false), Vst = gop(W.Bst, q, false);
     int ell = 0;
     double sest = 0.0;
     double flops = 0.0, bytes = 0.0;
     for (int round = 0;; ++round) {
-        // ---- probes Omega (q x RB) and zero Yn
-        for (int idx = threadIdx.x; idx < q * TR_RB; idx += blockDim.x)
-            Om[idx] = rnd_normal(seed + (uint64_t)round * 0x100000000ull + (uint64_t)idx);
-        for (int idx = threadIdx.x; idx < m * TR_RB; idx += blockDim.x) Yn[idx] = 0.0;
-        __syncthreads();
-        // ---- Yn = M Omega = sum_p alpha_p U_p (V_p^T Omega_rows)
-        for (int pi = 0; pi < t.piece_count; ++pi) {
-            const TPiece pc = pieces[t.piece_begin + pi];
-            const int w = dim_eval(pc.w, ranks);
-            if (w == 0) continue;
-            const double* U = pool + pc.u_off;
-            const double* V = pool + pc.v_off;
-            for (int c0 = 0; c0 < w; c0 += TR_WMAX_SM) {
-                const int wc = min(TR_WMAX_SM, w - c0);
-                for (int c = warp; c < wc; c += nw) {
-                    double acc[TR_RB];
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) acc[j] = 0.0;
-                    const double* vc = V + (int64_t)(c0 + c) * pc.v_ld;
-                    for (int i = lane; i < pc.v_rows; i += 32) {
-                        const double v = vc[i];
-                        const double* o = Om + pc.v_row0 + i;
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) acc[j] += v * o[(int64_t)j * q];
-                    }
-                    warp_sum_arr(acc);
-                    if (lane == 0)
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) Tp[c + j * TR_WMAX_SM] = acc[j];
-                }
-                __syncthreads();
-                for (int i = threadIdx.x; i < pc.u_rows; i += blockDim.x) {
-                    double acc[TR_RB];
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) acc[j] = 0.0;
-                    for (int c = 0; c < wc; ++c) {
-                        const double u = U[i + (int64_t)(c0 + c) * pc.u_ld];
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) acc[j] += u * Tp[c + j * TR_WMAX_SM];
-                    }
-                    double* y = Yn + pc.u_row0 + i;
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) y[(int64_t)j * m] += pc.alpha * acc[j];
-                }
-                __syncthreads();
+        // ---- R1: probes Omega (q x RB) in fixed row chunks, with partial column norms
+        for (int c = sub; c < nchq; c += nsub) {
+            const int r0 = c * TR_RCH, r1 = min(q, r0 + TR_RCH);
+            for (int idx = threadIdx.x; idx < (r1 - r0) * TR_RB; idx += blockDim.x) {
+                const int i = r0 + idx % (r1 - r0), j = idx / (r1 - r0);
+                W.Om[i + (int64_t)j * q] = rnd_normal(seed + (uint64_t)round * 0x100000000ull + (uint64_t)(i + j * q));
             }
-            flops += 4.0 * TR_RB * w * (double)(pc.u_rows + pc.v_rows);
-            bytes += 8.0 * w * (double)(pc.u_rows + pc.v_rows);
+            __syncthreads();
+            for (int j = warp; j < TR_RB; j += nw) {
+                double a = 0.0;
+                for (int i = r0 + lane; i < r1; i += 32) a += W.Om[i + (int64_t)j * q] * W.Om[i + (int64_t)j * q];
+                a = warp_sum(a);
+                if (lane == 0) W.npart[(int64_t)(nchm + c) * TR_RB + j] = a;
+            }
         }
-        // ---- sigma_1 lower bound: max_j ||Y_j|| / ||Omega_j||  (one warp per probe)
-        for (int j = warp; j < TR_RB; j += nw) {
-            double a = 0.0, b = 0.0;
-            for (int i = lane; i < m; i += 32) a += Yn[i + (int64_t)j * m] * Yn[i + (int64_t)j * m];
-            for (int i = lane; i < q; i += 32) b += Om[i + (int64_t)j * q] * Om[i + (int64_t)j * q];
-            a = warp_sum(a);
-            b = warp_sum(b);
-            if (lane == 0) s_ratio[j] = (b > 0.0) ? sqrt(a / b) : 0.0;
+        coop_sync(bar, nsub, gen, stt);            // Omega (and the gathered stacks) complete
+        // ---- R2: T^T = Omega^T V_stack  (16 x K)
+        gemm_short(TR_RB, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_RB, sub, nsub, gsm);
+        coop_sync(bar, nsub, gen, stt);
+        // ---- R3: Y = U_stack T  (m x 16)
+        gemm_narrow64(m, TR_RB, K, 1.0, Ust, gop(W.Tt, TR_RB, true), 0.0, W.Y, m, sub, nsub, gsm);
+        coop_sync(bar, nsub, gen, stt);
+        flops += 4.0 * TR_RB * (double)K * (m + q);
+        bytes += 8.0 * Srows;
+        for (int c = sub; c < nchm; c += nsub) {
+            const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+            for (int j = warp; j < TR_RB; j += nw) {
+                double a = 0.0;
+                for (int i = r0 + lane; i < r1; i += 32) a += W.Y[i + (int64_t)j * m] * W.Y[i + (int64_t)j * m];
+                a = warp_sum(a);
+                if (lane == 0) W.npart[(int64_t)c * TR_RB + j] = a;
+            }
+        }
+        coop_sync(bar, nsub, gen, stt);
+        // ---- scale: max_j ||M w_j|| over the probes seen so far (every CTA, same order)
+        if (threadIdx.x < TR_RB) {
+            const int j = threadIdx.x;
+            double a = 0.0;
+            for (int c = 0; c < nchm; ++c) a += __ldcg(W.npart + (int64_t)c * TR_RB + j);
+            s_ratio[j] = sqrt(a);
         }
         __syncthreads();
         for (int j = 0; j < TR_RB; ++j) sest = fmax(sest, s_ratio[j]);
-        const double thr = eps * sest * 0.125;
-        // ---- Yn <- (I - Q Q^T) Yn, twice
+        const double thr = eps * sest * TR_STOP;
+        __syncthreads();
+        // ---- R4 (row-owned, no leader loops): BCGS2 with a pivoted Cholesky-QR of the block
+        //   Y <- (I - Q Q^T) Y twice; G = Y^T Y; pivoted Cholesky of G with the
+        //   threshold -> selection P, R; Qn = Y_P R^-1; Qn <- (I - Q Q^T) Qn; CholQR of Qn.
+        // Partial reductions over each CTA's own 64-row chunks are summed by every CTA
+        // in the same order, so all CTAs take the same decisions without a broadcast.
         if (ell > 0) {
-            for (int pass = 0; pass < 2; ++pass) {
-                for (int l = warp; l < ell; l += nw) {
-                    double acc[TR_RB];
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) acc[j] = 0.0;
-                    const double* ql = Qm + (int64_t)l * m;
-                    for (int i = lane; i < m; i += 32) {
-                        const double qv = ql[i];
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) acc[j] += qv * Yn[i + (int64_t)j * m];
-                    }
-                    warp_sum_arr(acc);
-                    if (lane == 0)
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) Cs[l + j * TR_LMAX] = acc[j];
-                }
-                __syncthreads();
-                for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                    double acc[TR_RB];
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) acc[j] = 0.0;
-                    for (int l = 0; l < ell; ++l) {
-                        const double qv = Qm[i + (int64_t)l * m];
-#pragma unroll
-                        for (int j = 0; j < TR_RB; ++j) acc[j] += qv * Cs[l + j * TR_LMAX];
-                    }
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j) Yn[i + (int64_t)j * m] -= acc[j];
-                }
-                __syncthreads();
-            }
+            for (int pass = 0; pass < 2; ++pass) proj_owned(W, m, ell, L, W.Y, TR_RB, sub, nsub, nchm, bar, gen, stt, gsm);
             flops += 8.0 * TR_RB * (double)ell * m;
         }
-        // ---- column-pivoted MGS of the RB probes with re-orthogonalisation: take the
-        // probe with the largest residual norm while it exceeds thr, normalise it,
-        // project it out of the remaining probes (twice).  When it stops, every
-        // remaining probe residual is <= thr -- the certificate of the range finder.
-        if (threadIdx.x == 0) s_added = 0;
-        for (int j = threadIdx.x; j < TR_RB; j += blockDim.x) s_alive[j] = 1;
-        __syncthreads();
-        double maxn = 0.0;
-        for (int step = 0; step < TR_RB; ++step) {
-            for (int j = warp; j < TR_RB; j += nw) {
-                double a = 0.0;
-                if (s_alive[j])
-                    for (int i = lane; i < m; i += 32) a += Yn[i + (int64_t)j * m] * Yn[i + (int64_t)j * m];
-                a = warp_sum(a);
-                if (lane == 0) s_ratio[j] = s_alive[j] ? sqrt(a) : -1.0;
-            }
-            __syncthreads();
-            int jp = -1;
-            double best = -1.0;
-            for (int j = 0; j < TR_RB; ++j)
-                if (s_ratio[j] > best) { best = s_ratio[j]; jp = j; }
-            if (step == 0) maxn = best;
-            const int na = s_added;
-            if (!(best > thr) || ell + na >= L) break;
-            // re-orthogonalise the pivot against the whole basis (old + new), twice:
-            // its residual can be ~eps below its original norm, so the rounding of
-            // the earlier projections must be removed before normalising
-            double* yp = Yn + (int64_t)jp * m;
-            const int nb = ell + na;
-            for (int pass = 0; pass < 2 && nb > 0; ++pass) {
-                for (int l = warp; l < nb; l += nw) {
-                    const double* ql = Qm + (int64_t)l * m;
-                    double d = 0.0;
-                    for (int i = lane; i < m; i += 32) d += ql[i] * yp[i];
-                    d = warp_sum(d);
-                    if (lane == 0) Cs[l] = d;
-                }
-                __syncthreads();
-                for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                    double a = 0.0;
-                    for (int l = 0; l < nb; ++l) a += Qm[i + (int64_t)l * m] * Cs[l];
-                    yp[i] -= a;
-                }
-                __syncthreads();
-            }
-            double nn = 0.0;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) nn += yp[i] * yp[i];
-            const double nrm = sqrt(block_sum(nn, scratch));
-            if (!(nrm > thr)) {                    // only rounding left: drop the probe
-                if (threadIdx.x == 0) s_alive[jp] = 0;
-                __syncthreads();
-                continue;
-            }
-            double* qn = Qm + (int64_t)(ell + na) * m;
-            const double inv = 1.0 / nrm;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) qn[i] = yp[i] * inv;
-            __syncthreads();
-            if (threadIdx.x == 0) { s_alive[jp] = 0; s_added = na + 1; }
-            for (int j = warp; j < TR_RB; j += nw) {
-                if (j == jp || !s_alive[j]) continue;
-                double* y = Yn + (int64_t)j * m;
-                for (int pass = 0; pass < 2; ++pass) {
-                    double d = 0.0;
-                    for (int i = lane; i < m; i += 32) d += qn[i] * y[i];
-                    d = warp_sum(d);
-                    for (int i = lane; i < m; i += 32) y[i] -= d * qn[i];
-                    __syncwarp();
-                }
-            }
-            __syncthreads();
-        }
-        const int added = s_added;
-        flops += 4.0 * m * (double)TR_RB * TR_RB;
-        ell += added;
-        if (maxn <= thr || added == 0) break;      // every probe below eps sigma_est / 8
-        if (ell >= L) {                            // basis full: no room to certify the tolerance
-            if (threadIdx.x == 0) atomicOr(flags + 1, 2);
-            break;
-        }
-        if (ell >= m || ell >= q) break;           // basis spans the whole range
-    }
-    __syncthreads();
-    if (ell == 0) {
+        gram_owned(W, m, W.Y, TR_RB, sub, nsub, nchm, bar, gen, stt, gsm, Gs);
+        // pivoted Cholesky (redundant, identical in every CTA): accept pivots above
+        // max(thr, 1e-4 * largest) so R stays well conditioned (cond <= 1e4); weaker
+        // directions are picked up by the next round's probes
         if (threadIdx.x == 0) {
+            double d0 = 0.0;
+            for (int j = 0; j < TR_RB; ++j) { piv[j] = j; d0 = fmax(d0, Gs[j * TR_RB + j]); }
+            s_maxn = sqrt(fmax(d0, 0.0));
+            const double cut = fmax(thr * thr, 1e-8 * d0);
+            int na = 0;
+            for (int k = 0; k < TR_RB && ell + k < L; ++k) {
+                int jb = k;
+                for (int j = k + 1; j < TR_RB; ++j)
+                    if (Gs[piv[j] * TR_RB + piv[j]] > Gs[piv[jb] * TR_RB + piv[jb]]) jb = j;
+                const int tmp = piv[k]; piv[k] = piv[jb]; piv[jb] = tmp;
+                const int pk = piv[k];
+                const double d = Gs[pk * TR_RB + pk];
+                if (!(d > cut)) break;
+                const double rkk = sqrt(d);
+                Rs[k * TR_RB + k] = rkk;
+                for (int j = k + 1; j < TR_RB; ++j) Rs[k * TR_RB + j] = Gs[pk * TR_RB + piv[j]] / rkk;
+                for (int i = k + 1; i < TR_RB; ++i)        // trailing Schur complement (pivoted indices)
+                    for (int j = i; j < TR_RB; ++j) {
+                        const double v = Gs[piv[i] * TR_RB + piv[j]] - Rs[k * TR_RB + i] * Rs[k * TR_RB + j];
+                        Gs[piv[i] * TR_RB + piv[j]] = v;
+                        Gs[piv[j] * TR_RB + piv[i]] = v;
+                    }
+                ++na;
+            }
+            s_na = na;
+        }
+        __syncthreads();
+        const int na = s_na;
+        const double maxn = s_maxn;
+        if (na > 0) {
+            // Qn = Y_P R^-1 on the owned rows (thread per row, forward substitution)
+            for (int c = sub; c < nchm; c += nsub) {
+                const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+                for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                    double x[TR_RB];
+#pragma unroll
+                    for (int j = 0; j < TR_RB; ++j) {
+                        if (j < na) {
+                            double v = W.Y[i + (int64_t)piv[j] * m];
+                            for (int k = 0; k < j; ++k) v -= x[k] * Rs[k * TR_RB + j];
+                            x[j] = v / Rs[j * TR_RB + j];
+                            W.Q[i + (int64_t)(ell + j) * m] = x[j];
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            double* Qn = W.Q + (int64_t)ell * m;
+            if (ell > 0) proj_owned(W, m, ell, L, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm);
+            gram_owned(W, m, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm, Gs);
+            // CholQR of the (nearly orthonormal) new block: Qn <- Qn chol(Qn^T Qn)^-1
+            if (threadIdx.x == 0) {
+                for (int k = 0; k < na; ++k) {
+                    double d = Gs[k * TR_RB + k];
+                    for (int l = 0; l < k; ++l) d -= Rs[l * TR_RB + k] * Rs[l * TR_RB + k];
+                    const double rkk = sqrt(fmax(d, 1e-300));
+                    Rs[k * TR_RB + k] = rkk;
+                    for (int j = k + 1; j < na; ++j) {
+                        double v = Gs[k * TR_RB + j];
+                        for (int l = 0; l < k; ++l) v -= Rs[l * TR_RB + k] * Rs[l * TR_RB + j];
+                        Rs[k * TR_RB + j] = v / rkk;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int c = sub; c < nchm; c += nsub) {
+                const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+                for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                    double x[TR_RB];
+#pragma unroll
+                    for (int j = 0; j < TR_RB; ++j) {
+                        if (j < na) {
+                            double v = Qn[i + (int64_t)j * m];
+                            for (int k = 0; k < j; ++k) v -= x[k] * Rs[k * TR_RB + j];
+                            x[j] = v / Rs[j * TR_RB + j];
+                            Qn[i + (int64_t)j * m] = x[j];
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            flops += 4.0 * (double)na * ell * m + 6.0 * (double)na * na * m;
+        }
+        const int ell2 = ell + na;
+        bool done = (maxn <= thr) || na == 0;
+        if (!done && ell2 >= L) { done = true; if (sub == 0 && threadIdx.x == 0) atomicOr(flags + 1, 2); }
+        if (!done && (ell2 >= m || ell2 >= q)) done = true;
+        ell = ell2;
+        if (done || round > 64) break;
+    }
+    coop_sync(bar, nsub, gen, stt);                // basis Q complete on every row
+    if (ell == 0) {
+        if (sub == 0 && threadIdx.x == 0) {
             ranks[t.rslot] = 0;
             atomicAdd(ctr + CTR_TRUNC + 0, flops);
             atomicAdd(ctr + CTR_TRUNC + 1, bytes);
         }
+        coop_sync(bar, nsub, gen, stt);
         return;
     }
-    // ---- W = M^T Q = sum_p alpha_p V_p (U_p^T Q_rows)   (q x ell)
-    for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) Wm[idx] = 0.0;
-    __syncthreads();
-    for (int pi = 0; pi < t.piece_count; ++pi) {
-        const TPiece pc = pieces[t.piece_begin + pi];
-        const int w = dim_eval(pc.w, ranks);
-        if (w == 0) continue;
-        const double* U = pool + pc.u_off;
-        const double* V = pool + pc.v_off;
-        // P_p[c, l] = alpha * sum_i U[i, c] Q[u_row0 + i, l]   (w x ell, ld w), one warp per (c, l)
-        for (int pr = warp; pr < w * ell; pr += nw) {
-            const int c = pr % w, l = pr / w;
-            const double* uc = U + (int64_t)c * pc.u_ld;
-            const double* ql = Qm + (int64_t)l * m + pc.u_row0;
-            double d = 0.0;
-            for (int i = lane; i < pc.u_rows; i += 32) d += uc[i] * ql[i];
-            d = warp_sum(d);
-            if (lane == 0) Pp[c + (int64_t)l * w] = pc.alpha * d;
+    // ---- F1: P^T = Q^T U_stack  (ell x K);  F2: W = V_stack P  (q x ell)
+    gemm_wide(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
+    coop_sync(bar, nsub, gen, stt);
+    gemm_wide(q, ell, K, 1.0, Vst, gop(W.Pt, L, true), 0.0, W.Wm, q, sub, nsub, gsm);
+    coop_sync(bar, nsub, gen, stt);
+    flops += 4.0 * (double)ell * K * (m + q);
+    bytes += 8.0 * Srows;
+    const int Kw = min(q, ell);
+    if (sub == 0) {
+        // ---- F3 (leader): Householder QR of a copy of W, S = R^T, Jacobi S Z = X', rank, order
+        for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) W.Wc[idx] = W.Wm[idx];
+        __syncthreads();
+        house_qr(W.Wc, q, ell, W.tau, scratch);
+        for (int idx = threadIdx.x; idx < ell * Kw; idx += blockDim.x) {
+            const int i = idx % ell, j = idx / ell;
+            W.S[i + (int64_t)j * ell] = (i >= j) ? W.Wc[j + (int64_t)i * q] : 0.0;
         }
         __syncthreads();
-        // W[v_row0 + i, l] += sum_c V[i, c] P_p[c, l]
-        for (int i = threadIdx.x; i < pc.v_rows; i += blockDim.x) {
-            for (int l0 = 0; l0 < ell; l0 += TR_RB) {
-                const int lc = min(TR_RB, ell - l0);
-                double acc[TR_RB];
-#pragma unroll
-                for (int j = 0; j < TR_RB; ++j) acc[j] = 0.0;
-                for (int c = 0; c < w; ++c) {
-                    const double v = V[i + (int64_t)c * pc.v_ld];
-#pragma unroll
-                    for (int j = 0; j < TR_RB; ++j)
-                        if (j < lc) acc[j] += v * Pp[c + (int64_t)(l0 + j) * w];
-                }
-                for (int j = 0; j < lc; ++j) Wm[pc.v_row0 + i + (int64_t)(l0 + j) * q] += acc[j];
+        jacobi_svd(W.S, ell, Kw, W.Z, &s_flag);
+        for (int j = warp; j < Kw; j += nw) {
+            double sacc = 0.0;
+            for (int r = lane; r < ell; r += 32) sacc += W.S[r + (int64_t)j * ell] * W.S[r + (int64_t)j * ell];
+            sacc = warp_sum(sacc);
+            if (lane == 0) W.sig[j] = sqrt(sacc);
+        }
+        __syncthreads();
+        const int kk = min(Kw, ORDER_MAX);
+        for (int j = threadIdx.x; j < kk; j += blockDim.x) {
+            int pos = 0;
+            const double sj = W.sig[j];
+            for (int b2 = 0; b2 < kk; ++b2) pos += (W.sig[b2] > sj || (W.sig[b2] == sj && b2 < j)) ? 1 : 0;
+            order[pos] = j;
+        }
+        __syncthreads();
+        {
+            const double smax = W.sig[order[0]];
+            int cnt = 0;
+            for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (W.sig[j] > eps * smax && W.sig[j] > 0.0) ? 1 : 0;
+            const double tot = block_sum((double)cnt, scratch);
+            if (threadIdx.x == 0) {
+                int r = (int)(tot + 0.5);
+                if (r > cap) { atomicOr(flags + 1, 2); r = cap; }
+                s_rank = r;
+                ctl[2] = r;
             }
         }
         __syncthreads();
-        flops += 4.0 * (double)ell * w * (pc.u_rows + pc.v_rows);
-        bytes += 8.0 * w * (double)(pc.u_rows + pc.v_rows);
-    }
-    // ---- W = Q_W R;  S = R^T;  one-sided Jacobi S Z = X (orthogonal columns)
-    house_qr(Wm, q, ell, tau, scratch);
-    const int Kw = min(q, ell);
-    for (int idx = threadIdx.x; idx < ell * Kw; idx += blockDim.x) {
-        const int i = idx % ell, j = idx / ell;      // S[i][j] = R[j][i] (ell x Kw), R upper
-        S[i + (int64_t)j * ell] = (i >= j) ? Wm[j + (int64_t)i * q] : 0.0;
-    }
-    __syncthreads();
-    jacobi_svd(S, ell, Kw, Z, &s_flag);
-    for (int j = warp; j < Kw; j += nw) {
-        double s = 0.0;
-        for (int r = lane; r < ell; r += 32) s += S[r + (int64_t)j * ell] * S[r + (int64_t)j * ell];
-        s = warp_sum(s);
-        if (lane == 0) sig[j] = sqrt(s);
-    }
-    __syncthreads();
-    const int kk = min(Kw, ORDER_MAX);
-    for (int j = threadIdx.x; j < kk; j += blockDim.x) {
-        int pos = 0;
-        const double sj = sig[j];
-        for (int b = 0; b < kk; ++b) pos += (sig[b] > sj || (sig[b] == sj && b < j)) ? 1 : 0;
-        order[pos] = j;
-    }
-    __syncthreads();
-    {
-        const double smax = sig[order[0]];
-        int cnt = 0;
-        for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (sig[j] > eps * smax && sig[j] > 0.0) ? 1 : 0;
-        const double tot = block_sum((double)cnt, scratch);
-        if (threadIdx.x == 0) {
-            int r = (int)(tot + 0.5);
-            if (r > cap) { atomicOr(flags + 1, 2); r = cap; }
-            s_rank = r;
+        const int r = s_rank;
+        for (int idx = threadIdx.x; idx < ell * r; idx += blockDim.x) {   // Xo = X'(:, order), G = Xo / sigma^2
+            const int l = idx % ell, c = idx / ell;
+            const int oc = order[c];
+            const double x = W.S[l + (int64_t)oc * ell];
+            const double sg = W.sig[oc];
+            W.Xo[l + (int64_t)c * L] = x;
+            W.G[l + (int64_t)c * L] = x / (sg * sg);
         }
+        const double el = ell, qd = q, kw = Kw;
+        flops += 2.0 * (qd * el * kw - kw * kw * kw / 3.0) + 3.0 * kw * (kw - 1.0) * (el + kw);
     }
-    __syncthreads();
-    const int r = s_rank;
-    // U_out = Q S(:, order)   (m x r);  M^T ~ Q_W R Q^T  =>  M ~ Q R^T Q_W^T = Q (S Z^T) Q_W^T
+    coop_sync(bar, nsub, gen, stt);                // rank, Xo, G published
+    const int r = __ldcg(ctl + 2);
+    // ---- F4: U_out = Q Xo (m x r),  V_out = W G (q x r)
     double* Uo = pool + t.u_out;
     double* Vo = pool + t.v_out;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        for (int c = 0; c < r; ++c) {
-            const double* sc = S + (int64_t)order[c] * ell;
-            double s = 0.0;
-            for (int l = 0; l < ell; ++l) s += Qm[i + (int64_t)l * m] * sc[l];
-            Uo[i + (int64_t)c * m] = s;
-        }
+    if (r > 0) {
+        // tiles of the V product start where the U tiles left off, so idle CTAs take them first
+        const int tu = gemm_tiles(m, r, 64, 64);
+        gemm_wide(m, r, ell, 1.0, gop(W.Q, m, false), gop(W.Xo, L, false), 0.0, Uo, m, sub, nsub, gsm);
+        gemm_wide(q, r, ell, 1.0, gop(W.Wm, q, false), gop(W.G, L, false), 0.0, Vo, q, (sub + tu) % nsub, nsub, gsm);
     }
-    // V_out = Q_W [Z(:, order); 0]   (q x r)
-    for (int idx = threadIdx.x; idx < q * r; idx += blockDim.x) {
-        const int i = idx % q, c = idx / q;
-        Vo[i + (int64_t)c * q] = (i < Kw) ? Z[i + (int64_t)order[c] * Kw] : 0.0;
-    }
-    __syncthreads();
-    house_apply_q(Wm, q, Kw, tau, Vo, r);
-    if (threadIdx.x == 0) {
-        ranks[t.rslot] = r;
-        const double el = ell, qd = q, md = m, kw = Kw, rd = r;
-        flops += 2.0 * (qd * el * kw - kw * kw * kw / 3.0) + 3.0 * kw * (kw - 1.0) * (el + kw) + 2.0 * md * el * rd +
-                 4.0 * qd * kw * rd;
-        bytes += 8.0 * rd * (md + qd);
+    if (sub == 0 && threadIdx.x == 0) {
+        flops += 2.0 * (double)r * ell * (m + q);
+        bytes += 8.0 * (double)r * (m + q);
         atomicAdd(ctr + CTR_TRUNC + 0, flops);
         atomicAdd(ctr + CTR_TRUNC + 1, bytes);
     }
+    coop_sync(bar, nsub, gen, stt);                // all output rows written before the leader publishes
+    if (sub == 0 && threadIdx.x == 0) ranks[t.rslot] = r;
 }
 
 // dynamic shared memory (bytes) the truncation needs
-constexpr int TR_SMEM = (TR_WMAX_SM * TR_RB + TR_LMAX * TR_RB) * 8 + ORDER_MAX * 4;
+constexpr int TR_SMEM = TR_SMEM_A + ORDER_MAX * 4 + (TR_PMAX + 1) * 4;
 
+// sub / nsub / bar: this CTA's index in a cooperative truncation (nsub CTAs,
+// persistent executor only), else 0 / 1 / nullptr
 __device__ __forceinline__ void trunc_run(const TTask& t, const TPiece* __restrict__ pieces, double* pool, int* ranks,
-                                          int* flags, double eps, double* ctr, double* dsm) {
+                                          int* flags, double eps, double* ctr, double* dsm, int sub = 0, int nsub = 1,
+                                          int* bar = nullptr, unsigned long long* stt = nullptr) {
     int K = 0;
     for (int p = 0; p < t.piece_count; ++p) K += dim_eval(pieces[t.piece_begin + p].w, ranks);
     if (t.kmax_tot <= TR_EXACT_K) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
-    else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
+    else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr, dsm, sub, nsub, bar, stt);
 }
 
 }  // namespace hm

@@ -16,6 +16,7 @@ from __future__ import annotations
 import math
 
 import numpy as np
+import scipy.linalg
 
 from oracle.matern import matern
 
@@ -26,7 +27,7 @@ VINS = np.dtype([("op", "u1"), ("t0", "u1"), ("t1", "u1"), ("t2", "u1"), ("ta", 
 VTASK = np.dtype([("ins_begin", "<i4"), ("ins_count", "<i4")])
 TTASK = np.dtype([("u_out", "<i8"), ("v_out", "<i8"), ("ws", "<i8"), ("ws_size", "<i8"), ("m", "<i4"),
                   ("q", "<i4"), ("cap", "<i4"), ("rslot", "<i4"), ("piece_begin", "<i4"), ("piece_count", "<i4"),
-                  ("kmax_tot", "<i4"), ("pad", "<i4")])
+                  ("kmax_tot", "<i4"), ("wmax", "<i4"), ("nsub", "<i4"), ("bar", "<i4")])
 TPIECE = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("u_ld", "<i4"), ("v_ld", "<i4"), ("u_row0", "<i4"),
                    ("u_rows", "<i4"), ("v_row0", "<i4"), ("v_rows", "<i4"), ("w", DIM), ("alpha", "<f8")])
 DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4")])
@@ -49,7 +50,8 @@ def _read(path):
     return out
 
 
-XTASK = np.dtype([("kind", "<i4"), ("idx", "<i4"), ("dep_begin", "<i4"), ("dep_count", "<i4")])
+XTASK = np.dtype([("kind", "<i4"), ("idx", "<i4"), ("dep_begin", "<i4"), ("dep_count", "<i4"), ("sub", "<i4"),
+                  ("nsub", "<i4")])
 
 
 class Phase:
@@ -243,7 +245,7 @@ class Interp:
             x = ph.xt[i]
             if x["kind"] == 0:
                 self.vm(ph, ph.vt[x["idx"]])
-            else:
+            elif x["sub"] == 0:              # a cooperative truncation runs once (its leader)
                 self.trunc(ph, ph.tt[x["idx"]])
             done += 1
             for s2 in succ[i]:
@@ -279,9 +281,13 @@ class Interp:
 
 class InterpRand(Interp):
     """Interp whose wide truncations follow the device's randomized range finder
-    (trunc.cuh, trunc_rand) step by step: rounds of RB Gaussian probes, twice
-    projected against Q, column-pivoted MGS with threshold eps * sigma_est / 8,
-    then W = M^T Q, QR, SVD.  Used to check that algorithm on the CPU."""
+    (trunc.cuh, trunc_rand) step by step: rounds of RB Gaussian probes, block
+    Gram-Schmidt twice (BCGS2) with a pivoted Cholesky-QR of each block (pivots
+    above max(eps * max_j ||M w_j||, 1e-4 * largest)) and a CholQR of the
+    re-projected block, stopping when the largest projected probe is below
+    eps * max_j ||M w_j|| (relative Frobenius certificate), then
+    W = M^T Q, QR, SVD of R^T,
+    U = Q X', V = W X' Sigma^-2.  Used to check that algorithm on the CPU."""
     RB = 16
     EXACT_K = 160
 
@@ -305,46 +311,53 @@ class InterpRand(Interp):
         while True:
             Om = self.rng.standard_normal((q, self.RB))
             Y = A @ (B.T @ Om)
-            sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0) / np.linalg.norm(Om, axis=0))))
-            thr = self.eps * sest / 8
-            for _ in range(2):
+            sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0))))   # ~ ||M||_F
+            thr = self.eps * sest * 1.0          # TR_STOP: relative Frobenius certificate
+            for _ in range(2):                       # BCGS2, first projection (twice)
                 Y = Y - Q @ (Q.T @ Y)
-            alive = list(range(self.RB))
-            added = []
-            maxn = None
-            while alive:
-                nr = [np.linalg.norm(Y[:, j]) for j in alive]
-                jb = int(np.argmax(nr))
-                best = nr[jb]
-                if maxn is None:
-                    maxn = best
-                if not best > thr or Q.shape[1] + len(added) >= L:
+            G = Y.T @ Y                              # pivoted Cholesky-QR of the block
+            d0 = float(np.max(np.diag(G)))
+            maxn = math.sqrt(max(d0, 0.0))
+            cut = max(thr * thr, 1e-8 * d0)
+            piv = list(range(self.RB))
+            R = np.zeros((self.RB, self.RB))
+            na = 0
+            for k in range(self.RB):
+                if Q.shape[1] + k >= L:
                     break
-                jp = alive.pop(jb)
-                Qc = np.concatenate([Q] + ([np.stack(added, 1)] if added else []), axis=1)
-                y = Y[:, jp].copy()
-                for _ in range(2):                      # re-orthogonalise against the whole basis
-                    y -= Qc @ (Qc.T @ y)
-                nrm = np.linalg.norm(y)
-                if not nrm > thr:
-                    continue
-                qn = y / nrm
-                added.append(qn)
-                for j in alive:
-                    for _ in range(2):
-                        Y[:, j] -= (qn @ Y[:, j]) * qn
-            if added:
-                Q = np.concatenate([Q, np.stack(added, 1)], axis=1)
+                jb = k + int(np.argmax([G[piv[j], piv[j]] for j in range(k, self.RB)]))
+                piv[k], piv[jb] = piv[jb], piv[k]
+                d = G[piv[k], piv[k]]
+                if not d > cut:
+                    break
+                R[k, k] = math.sqrt(d)
+                for j in range(k + 1, self.RB):
+                    R[k, j] = G[piv[k], piv[j]] / R[k, k]
+                for i in range(k + 1, self.RB):
+                    for j in range(i, self.RB):
+                        v = G[piv[i], piv[j]] - R[k, i] * R[k, j]
+                        G[piv[i], piv[j]] = v
+                        G[piv[j], piv[i]] = v
+                na += 1
+            added = []
+            if na:
+                Qn = scipy.linalg.solve_triangular(R[:na, :na], Y[:, piv[:na]].T, trans="T", lower=False).T
+                Qn = Qn - Q @ (Q.T @ Qn)             # second projection of the new block
+                R2 = np.linalg.cholesky(Qn.T @ Qn).T  # CholQR of the nearly orthonormal block
+                Qn = scipy.linalg.solve_triangular(R2, Qn.T, trans="T", lower=False).T
+                Q = np.concatenate([Q, Qn], axis=1)
+                added = [0] * na
             if maxn <= thr or not added or Q.shape[1] >= L or Q.shape[1] >= m or Q.shape[1] >= q:
                 break
         if Q.shape[1] == 0:
             self.ranks[t["rslot"]] = 0
             return
-        W = B @ (A.T @ Q)                       # M^T Q
-        Qw, R = np.linalg.qr(W)
-        X, S, Zt = np.linalg.svd(R.T)           # R^T = X S Z^T
+        Wm = B @ (A.T @ Q)                           # W = M^T Q
+        _, R = np.linalg.qr(Wm)
+        Xp, S, Zt = np.linalg.svd(R.T)               # R^T = X' Z^T with X' = Xp S
         r = int(np.sum((S > self.eps * S[0]) & (S > 0)))
         r = min(r, cap)
-        self.gstore(int(t["u_out"]), m, (Q @ X[:, :r]) * S[:r])
-        self.gstore(int(t["v_out"]), q, Qw @ Zt[:r].T)
+        Xr = Xp[:, :r] * S[:r]
+        self.gstore(int(t["u_out"]), m, Q @ Xr)                  # U = Q X'
+        self.gstore(int(t["v_out"]), q, Wm @ (Xr / S[:r] ** 2))   # V = W X' Sigma^-2 (= Q_W Z)
         self.ranks[t["rslot"]] = r

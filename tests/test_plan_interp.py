@@ -50,7 +50,7 @@ def test_randomized_truncation_algorithm(tmp_path, eps, tol):
     """The device's randomized range-finder truncation (trunc.cuh), replayed with
     numpy on the wide Cholesky truncations, keeps the likelihood at the accuracy
     eps allows (n = 2000, leaf 32: stacked widths reach ~1700 columns).  At
-    eps = 1e-10 this needs the full re-orthogonalisation of each new basis vector."""
+    eps = 1e-10 this needs the second projection of each new block (BCGS2)."""
     pts = uniform_iid(2000, 11)
     ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), 32, 2.0, eps, kmax=160, seed=0, k=1,
                                          cls=InterpRand)

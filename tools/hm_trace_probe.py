@@ -14,8 +14,8 @@ H.cholesky()
 H.assemble(theta)
 H.trace(True)
 H.cholesky()
-H.trace(False, f"gpurun_out/trace_{which}.bin")
+H.trace(False, f"/tmp/trace_{which}.bin")
 T = hm.Tree(pts, leaf, 2.0)
 T.plan_dump(f"/tmp/plan_{which}.bin", 160)
 print(H.timings())
-print(analyse(f"/tmp/plan_{which}.bin", f"gpurun_out/trace_{which}.bin", "chol", grid=296))
+print(analyse(f"/tmp/plan_{which}.bin", f"/tmp/trace_{which}.bin", "chol", grid=296))

@@ -18,9 +18,11 @@ from plan_interp import Plan  # noqa: E402
 def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 296, top: int = 15) -> str:
     P = Plan(plan_path)
     ph = getattr(P, phase)
-    tr = np.fromfile(trace_path, dtype=np.uint64).reshape(-1, 4)
+    raw = np.fromfile(trace_path, dtype=np.uint64)
     n = len(ph.xt)
-    assert tr.shape[0] == n, (tr.shape, n)
+    assert raw.size == 68 * n, (raw.size, n)
+    tr = raw[:4 * n].reshape(n, 4)
+    stg = raw[4 * n:].reshape(n, 64)
     t0 = tr[:, 0].min()
     claim = (tr[:, 0] - t0).astype(np.float64) * 1e-3   # us
     ready = (tr[:, 1] - t0).astype(np.float64) * 1e-3
@@ -57,6 +59,18 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
     lines.append(f"  critical path: {cp.max() / 1e3:.3f} ms over {len(path)} tasks "
                  f"(vm {int((pk == 0).sum())}: {dur[path][pk == 0].sum() / 1e3:.3f} ms, "
                  f"trunc {int((pk == 1).sum())}: {dur[path][pk == 1].sum() / 1e3:.3f} ms)")
+    # stage breakdown of the randomized truncations (leader stamps)
+    tsel = np.nonzero((kind == 1) & (stg[:, 0] > 0))[0]
+    if tsel.size:
+        lines.append("  randomized truncation stages (leader), us: [start->sync1, sync1->sync2, ...]")
+        single = tsel[ph.xt["nsub"][tsel] == 1]
+        pick = list(tsel[np.argsort(-dur[tsel])][:6]) + list(single[np.argsort(-dur[single])][:6])
+        for i in pick:
+            st = stg[i]
+            k = int(np.max(np.nonzero(st)[0]))
+            d = np.diff(st[:k + 1].astype(np.float64)) * 1e-3
+            x = ph.xt[i]; t = ph.tt[x["idx"]]
+            lines.append(f"    m={t['m']} q={t['q']} nsub={x['nsub']} total={dur[i]:.0f}: " + " ".join(f"{v:.0f}" for v in d))
     order = np.argsort(-dur)[:top]
     lines.append("  longest tasks:")
     for i in order:
