@@ -193,6 +193,7 @@ int hm_plan_dump(hm_tree t, int32_t kmax, const char* path, double summary[8]) {
                 put(ph->t_wave_begin.data(), (int64_t)ph->t_wave_begin.size(), 4);
                 put(ph->xt.data(), (int64_t)ph->xt.size(), sizeof(XTask));
                 put(ph->xdeps.data(), (int64_t)ph->xdeps.size(), 4);
+                put(ph->terms.data(), (int64_t)ph->terms.size(), sizeof(VTerm));
             }
             std::fclose(f);
         }

@@ -26,7 +26,7 @@ constexpr int EXEC_SMEM = (NTILE * TSZ * 8 > TR_SMEM) ? NTILE * TSZ * 8 : TR_SME
 
 __global__ void __launch_bounds__(TTHREADS, 2)
     k_exec(const XTask* __restrict__ xt, int nx, const int32_t* __restrict__ deps, const VTask* __restrict__ vt,
-           const VIns* __restrict__ ins, const TTask* __restrict__ tt, const TPiece* __restrict__ tp, double* pool,
+           const VIns* __restrict__ ins, const VTerm* __restrict__ terms, const TTask* __restrict__ tt, const TPiece* __restrict__ tp, double* pool,
            int* ranks, int* flags, double* ctr, double eps, int* done, int* counter, int epoch,
            unsigned long long* trace, int* bars) {
     extern __shared__ double sm[];
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         }
         __syncthreads();
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
-        if (x.kind == 0) vm_run(vt[x.idx], ins, pool, ranks, flags, ctr, sm);
+        if (x.kind == 0) vm_run(vt[x.idx], ins, terms, pool, ranks, flags, ctr, sm);
         else {
             const TTask t = tt[x.idx];
             trunc_run(t, tp, pool, ranks, flags, eps, ctr, sm, x.sub, x.nsub, bars + t.bar,
@@ -91,14 +91,15 @@ int exec_grid() {
     return grid;
 }
 
-void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
+void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const VTerm* terms,
+                 const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
                  int* counter, int epoch, unsigned long long* trace, int* bars, int nbars, cudaStream_t st) {
     if (nx <= 0) return;
     const int grid = exec_grid();
     HM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), st));
     if (nbars > 0) HM_CUDA_TRY(cudaMemsetAsync(bars, 0, sizeof(int) * nbars, st));
-    k_exec<<<grid, TTHREADS, EXEC_SMEM, st>>>(xt, nx, deps, vt, ins, tt, tp, pool, ranks, flags, ctr, eps, done,
+    k_exec<<<grid, TTHREADS, EXEC_SMEM, st>>>(xt, nx, deps, vt, ins, terms, tt, tp, pool, ranks, flags, ctr, eps, done,
                                               counter, epoch, trace, bars);
 }
 

@@ -163,10 +163,11 @@ __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__
 
 // ---------------------------------------------------------------- tile VM
 __global__ void __launch_bounds__(TTHREADS) k_vm(const VTask* __restrict__ tasks, const VIns* __restrict__ ins,
-                                                 double* __restrict__ pool, const int* __restrict__ ranks,
-                                                 int* __restrict__ flags, double* __restrict__ ctr) {
+                                                 const VTerm* __restrict__ terms, double* __restrict__ pool,
+                                                 const int* __restrict__ ranks, int* __restrict__ flags,
+                                                 double* __restrict__ ctr) {
     extern __shared__ double sm[];
-    vm_run(tasks[blockIdx.x], ins, pool, ranks, flags, ctr, sm);
+    vm_run(tasks[blockIdx.x], ins, terms, pool, ranks, flags, ctr, sm);
 }
 
 // ---------------------------------------------------------------- permutation / finish
@@ -224,9 +225,9 @@ void vm_set_attr() {
     HM_CUDA_TRY(cudaFuncSetAttribute(k_vm, cudaFuncAttributeMaxDynamicSharedMemorySize, NTILE * TSZ * 8));
     done = true;
 }
-void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, double* ctr,
-               cudaStream_t st) {
-    if (n > 0) k_vm<<<n, TTHREADS, NTILE * TSZ * 8, st>>>(t, ins, pool, ranks, flags, ctr);
+void launch_vm(const VTask* t, int n, const VIns* ins, const VTerm* terms, double* pool, const int* ranks, int* flags,
+               double* ctr, cudaStream_t st) {
+    if (n > 0) k_vm<<<n, TTHREADS, NTILE * TSZ * 8, st>>>(t, ins, terms, pool, ranks, flags, ctr);
 }
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st) {
     const int64_t tot = n * zw;

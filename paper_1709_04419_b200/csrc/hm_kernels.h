@@ -15,10 +15,11 @@ void launch_aca(const AcaTask* t, int n, const double* pts, double* pool, int* r
 void launch_trunc(const TTask* t, int n, const TPiece* pc, double* pool, int* ranks, int* flags, double eps,
                   double* ctr, cudaStream_t st);
 void vm_set_attr();
-void launch_vm(const VTask* t, int n, const VIns* ins, double* pool, const int* ranks, int* flags, double* ctr,
-               cudaStream_t st);
+void launch_vm(const VTask* t, int n, const VIns* ins, const VTerm* terms, double* pool, const int* ranks, int* flags,
+               double* ctr, cudaStream_t st);
 int exec_grid();
-void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const TTask* tt,
+void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const VTerm* terms,
+                 const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,
                  int* counter, int epoch, unsigned long long* trace, int* bars, int nbars, cudaStream_t st);
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st);

@@ -23,6 +23,8 @@ enum VmOp : uint8_t {
     VM_TRSM_LN = 6,  // tile[t0] <- tile[t1]^{-1} tile[t0]
     VM_TRMM_LN = 7,  // tile[t0] <- tile[t1] tile[t0]
     VM_ZERO = 8,     // tile[t0] <- 0 with dims (rows x cols)
+    VM_MGEMM = 9,    // tile[t0] += sum_i alpha_i op(A_i) op(B_i) over terms[goff .. goff+ld), A_i/B_i
+                     // streamed from the pool (pipelined DMMA; replaces LD, LD, GEMM triples)
 };
 constexpr int NTILE = 3;   // target + two operands (TRSM/TRMM reuse tile 1 for L)
 
@@ -43,6 +45,17 @@ struct VIns {
     int32_t pad2;
     double alpha, beta;
 };
+
+// One term of VM_MGEMM: op(A) (M x K) times op(B) (K x N), A/B given like a VM_LD
+// (pool offset, leading dimension, stored rows x cols), zero outside those dims.
+struct VTerm {
+    int64_t a_off, b_off;
+    Dim a_rows, a_cols, b_rows, b_cols;
+    int32_t a_ld, b_ld;
+    uint8_t ta, tb, pad0, pad1, pad2, pad3, pad4, pad5;
+    double alpha;
+};
+constexpr int VM_MAX_TERMS = 64;   // terms per VM_MGEMM instruction
 
 struct VTask {
     int32_t ins_begin;

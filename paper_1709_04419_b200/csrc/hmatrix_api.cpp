@@ -27,7 +27,7 @@ namespace hm {
 enum KFamily { KF_DGEN = 0, KF_ACA = 1, KF_TRUNC = 2, KF_VM = 3, KF_AUX = 4, KF_EXEC = 5, KF_N = 6 };
 
 struct DPhase {
-    DevBuf ins, vt, tt, tp, xt, xd;
+    DevBuf ins, vt, tt, tp, xt, xd, terms;
     const Phase* ph = nullptr;
 };
 
@@ -87,6 +87,7 @@ void upload_phase(DPhase& d, const Phase& p, cudaStream_t st) {
     upload(d.tt, p.tt, st);
     upload(d.tp, p.tp, st);
     upload(d.xt, p.xt, st);
+    upload(d.terms, p.terms, st);
     upload(d.xd, p.xdeps, st);
     d.ph = &p;
 }
@@ -126,7 +127,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         if (h->tracing)
             HM_CUDA_TRY(cudaMemsetAsync((char*)h->trace.p + 32 * p.xt.size(), 0, 8 * 64 * p.xt.size(), h->stream));
         launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
-                    d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
+                    d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
                     h->counter.as<int>(), h->epoch,
                     h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(), p.n_bars, h->stream);
         if (h->tracing) h->trace_n = (int64_t)p.xt.size();
@@ -143,7 +144,8 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         }
         if (v1 > v0) {
             Launch L(h, KF_VM);
-            launch_vm(d.vt.as<VTask>() + v0, v1 - v0, d.ins.as<VIns>(), pool, ranks, flags, ctr, h->stream);
+            launch_vm(d.vt.as<VTask>() + v0, v1 - v0, d.ins.as<VIns>(), d.terms.as<VTerm>(), pool, ranks, flags, ctr,
+                      h->stream);
         }
     }
     HM_CUDA_TRY(cudaGetLastError());

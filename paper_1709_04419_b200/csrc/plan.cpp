@@ -140,6 +140,40 @@ struct Builder {
         return w;
     }
 
+    // Peephole: every "LD t1 <- A; LD t2 <- B; GEMM t0 += alpha op(t1) op(t2)" triple becomes a
+    // term of one VM_MGEMM on t0 (consecutive triples on the same t0 share the instruction),
+    // so the device streams the operands through a pipelined DMMA loop instead of
+    // loading, synchronising and multiplying tile by tile.
+    static void fuse_mgemm(const std::vector<VIns>& in, std::vector<VIns>& out, std::vector<VTerm>& terms) {
+        size_t i = 0;
+        while (i < in.size()) {
+            auto is_triple = [&](size_t j) {
+                return j + 2 < in.size() && in[j].op == VM_LD && in[j + 1].op == VM_LD && in[j + 2].op == VM_GEMM &&
+                       in[j + 2].t1 == in[j].t0 && in[j + 2].t2 == in[j + 1].t0 && in[j].t0 != in[j + 1].t0 &&
+                       in[j + 2].beta == 1.0 && in[j + 2].t0 != in[j].t0 && in[j + 2].t0 != in[j + 1].t0;
+            };
+            if (!is_triple(i)) {
+                out.push_back(in[i]);
+                ++i;
+                continue;
+            }
+            VIns m = in[i + 2];
+            m.op = VM_MGEMM;
+            m.goff = (int64_t)terms.size();
+            m.ld = 0;
+            while (is_triple(i) && in[i + 2].t0 == m.t0 && m.ld < VM_MAX_TERMS) {
+                VTerm tm{};
+                tm.a_off = in[i].goff; tm.a_ld = in[i].ld; tm.a_rows = in[i].rows; tm.a_cols = in[i].cols;
+                tm.b_off = in[i + 1].goff; tm.b_ld = in[i + 1].ld; tm.b_rows = in[i + 1].rows; tm.b_cols = in[i + 1].cols;
+                tm.ta = in[i + 2].ta; tm.tb = in[i + 2].tb; tm.alpha = in[i + 2].alpha;
+                terms.push_back(tm);
+                ++m.ld;
+                i += 3;
+            }
+            out.push_back(m);
+        }
+    }
+
     void emit_vm(Prog& pg) {
         if (pg.ins.empty()) return;
         std::sort(pg.reads.begin(), pg.reads.end());
@@ -150,8 +184,8 @@ struct Builder {
         int32_t w = wave_of(pg.reads, pg.writes, deps);
         VTask t;
         t.ins_begin = (int32_t)ph->ins.size();
-        t.ins_count = (int32_t)pg.ins.size();
-        ph->ins.insert(ph->ins.end(), pg.ins.begin(), pg.ins.end());
+        fuse_mgemm(pg.ins, ph->ins, ph->terms);
+        t.ins_count = (int32_t)ph->ins.size() - t.ins_begin;
         xraw.push_back({w, 0, (int32_t)vraw.size(), std::move(deps)});
         vraw.push_back({w, t});
         ++n_tasks;

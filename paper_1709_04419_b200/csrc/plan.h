@@ -40,6 +40,7 @@ struct Thin {
 
 struct Phase {                   // one executable phase (levelled task lists)
     std::vector<VIns> ins;
+    std::vector<VTerm> terms;    // VM_MGEMM terms
     std::vector<VTask> vt;       // sorted by wave
     std::vector<TTask> tt;       // sorted by wave
     std::vector<TPiece> tp;

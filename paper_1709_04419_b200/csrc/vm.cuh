@@ -7,13 +7,139 @@
 #include "dev_util.cuh"
 #include "hm_kernels.h"
 #include "hm_tasks.h"
+#include "gemm.cuh"
 #include "tile.cuh"
 
 namespace hm {
 
+// VM_MGEMM: T0 (64 x 64 smem tile) += sum_t alpha_t op(A_t) op(B_t).  The (term, 16-wide
+// K chunk) sequence of all terms is streamed global -> shared memory through a
+// GM_NS-stage cp.async pipeline (zero-filled outside each operand's dims) into
+// `stage` (the free tiles 1..2), and accumulated in registers by the FP64 tensor
+// cores (warp tile 16 x 32, 4 x 2 warps); T0 is updated once at the end.
+struct TermRt {
+    const double* a;
+    const double* b;
+    int32_t lda, ldb, M, N, K, ch0;   // op(A) M x K, op(B) K x N; first chunk index
+    int32_t ta, tb;
+    double alpha;
+};
+
+__device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ terms, int nt, const double* pool,
+                                         const int* ranks, double* stage, double& c_fl, double& c_by) {
+    constexpr int LA = 65, LB = 65, SA = GM_BK * LA, SB = GM_BK * LB;
+    __shared__ TermRt tr[VM_MAX_TERMS];
+    __shared__ int s_nch;
+    if (threadIdx.x < nt) {
+        const VTerm v = terms[threadIdx.x];
+        const int ar = dim_eval(v.a_rows, ranks), ac = dim_eval(v.a_cols, ranks);
+        const int br = dim_eval(v.b_rows, ranks), bc = dim_eval(v.b_cols, ranks);
+        TermRt r;
+        r.a = pool + v.a_off;
+        r.b = pool + v.b_off;
+        r.lda = v.a_ld;
+        r.ldb = v.b_ld;
+        r.ta = v.ta;
+        r.tb = v.tb;
+        r.M = v.ta ? ac : ar;
+        r.N = v.tb ? br : bc;
+        const int ka = v.ta ? ar : ac, kb = v.tb ? bc : br;
+        r.K = ka < kb ? ka : kb;
+        r.alpha = v.alpha;
+        tr[threadIdx.x] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int t = 0; t < nt; ++t) {
+            tr[t].ch0 = c;
+            c += (tr[t].K + GM_BK - 1) / GM_BK;
+            c_fl += 2.0 * tr[t].M * tr[t].N * tr[t].K;
+            c_by += 8.0 * ((double)tr[t].M + tr[t].N) * tr[t].K;
+        }
+        s_nch = c;
+    }
+    __syncthreads();
+    const int nch = s_nch;
+    double* As = stage;
+    double* Bs = stage + GM_NS * SA;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    int it = 0;                                          // issue cursor: term / chunk within it
+    int ik = 0;
+    auto issue = [&](int s) {
+        while (it < nt && ik >= (tr[it].K + GM_BK - 1) / GM_BK) { ++it; ik = 0; }
+        const TermRt r = tr[it];
+        const int k0 = ik * GM_BK;
+        double* as = As + (s % GM_NS) * SA;
+        double* bs = Bs + (s % GM_NS) * SB;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = threadIdx.x + e * 256;     // 1024 = 64 x 16
+            int i, k;
+            if (r.ta) { k = idx % GM_BK; i = idx / GM_BK; } else { i = idx % 64; k = idx / 64; }
+            const bool ok = i < r.M && k0 + k < r.K;
+            cp_async8(as + k * LA + i, ok ? (r.ta ? r.a + (k0 + k) + (int64_t)i * r.lda : r.a + i + (int64_t)(k0 + k) * r.lda) : r.a,
+                      ok);
+            int j, kb;
+            if (r.tb) { j = idx % 64; kb = idx / 64; } else { kb = idx % GM_BK; j = idx / GM_BK; }
+            const bool okb = j < r.N && k0 + kb < r.K;
+            cp_async8(bs + kb * LB + j,
+                      okb ? (r.tb ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b + (k0 + kb) + (int64_t)j * r.ldb) : r.b, okb);
+        }
+        ++ik;
+    };
+    int ct = 0, ck = 0;                                  // compute cursor
+#pragma unroll
+    for (int s = 0; s < GM_NS - 1; ++s) {
+        if (s < nch) issue(s);
+        cp_async_commit();
+    }
+    for (int s = 0; s < nch; ++s) {
+        cp_async_wait<GM_NS - 2>();
+        __syncthreads();
+        if (s + GM_NS - 1 < nch) issue(s + GM_NS - 1);
+        cp_async_commit();
+        while (ct < nt && ck >= (tr[ct].K + GM_BK - 1) / GM_BK) { ++ct; ck = 0; }
+        const double al = tr[ct].alpha;
+        ++ck;
+        const double* as = As + (s % GM_NS) * SA;
+        const double* bs = Bs + (s % GM_NS) * SB;
+#pragma unroll
+        for (int kk = 0; kk < GM_BK; kk += 4) {
+            double af[2], bf[4];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) af[a] = al * as[(kk + t4) * LA + wm + a * 8 + g];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = bs[(kk + t4) * LB + wn + b * 8 + g];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma_884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = wm + a * 8 + g, c = wn + b * 8 + 2 * t4;
+            T0[c * TLD + r] += acc[a][b][0];
+            T0[(c + 1) * TLD + r] += acc[a][b][1];
+        }
+    __syncthreads();
+}
+
 // Execute one tile-VM program with the CTA (TTHREADS threads); sm = NTILE tiles.
-__device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict__ ins, double* pool, const int* ranks,
-                                       int* flags, double* ctr, double* sm) {
+__device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict__ ins, const VTerm* __restrict__ terms,
+                                       double* pool, const int* ranks, int* flags, double* ctr, double* sm) {
     __shared__ int trows[NTILE], tcols[NTILE];
     __shared__ double s_log;
     double c_fl = 0.0, c_by = 0.0;   // algorithmic flops / bytes of this program (thread 0)
@@ -32,6 +158,9 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
                 tile_store(T0, pool + I.goff, I.ld, min(r, trows[I.t0]), min(c, tcols[I.t0]));
                 if (threadIdx.x == 0) c_by += 8.0 * min(r, trows[I.t0]) * min(c, tcols[I.t0]);
                 __syncthreads();
+            } break;
+            case VM_MGEMM: {
+                vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + TSZ, c_fl, c_by);
             } break;
             case VM_ZERO: {
                 tile_zero(T0);

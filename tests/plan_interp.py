@@ -34,7 +34,7 @@ DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q
 ACA = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4"),
                 ("cap", "<i4"), ("rslot", "<i4")])
 
-VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO = range(1, 9)
+VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM = range(1, 10)
 TD = 64
 
 
@@ -50,6 +50,9 @@ def _read(path):
     return out
 
 
+VTERM = np.dtype([("a_off", "<i8"), ("b_off", "<i8"), ("a_rows", DIM), ("a_cols", DIM), ("b_rows", DIM),
+                  ("b_cols", DIM), ("a_ld", "<i4"), ("b_ld", "<i4"), ("ta", "u1"), ("tb", "u1"), ("p", "u1", (6,)),
+                  ("alpha", "<f8")])
 XTASK = np.dtype([("kind", "<i4"), ("idx", "<i4"), ("dep_begin", "<i4"), ("dep_count", "<i4"), ("sub", "<i4"),
                   ("nsub", "<i4")])
 
@@ -57,8 +60,9 @@ XTASK = np.dtype([("kind", "<i4"), ("idx", "<i4"), ("dep_begin", "<i4"), ("dep_c
 class Phase:
     def __init__(self, secs):
         (ni, si, bi), (nv, sv, bv), (nt, st, bt), (np_, sp, bp), (nw1, _, bw1), (nw2, _, bw2), (nx, sx, bx), \
-            (nd, _, bd) = secs
-        assert sx == XTASK.itemsize
+            (nd, _, bd), (nm, sm_, bm) = secs
+        assert sx == XTASK.itemsize and (nm == 0 or sm_ == VTERM.itemsize)
+        self.terms = np.frombuffer(bm, VTERM, nm)
         self.xt = np.frombuffer(bx, XTASK, nx)
         self.xdeps = np.frombuffer(bd, "<i4", nd)
         assert si == VINS.itemsize and sv == VTASK.itemsize and st == TTASK.itemsize and sp == TPIECE.itemsize
@@ -79,7 +83,7 @@ class Plan:
         assert secs[1][1] == DGEN.itemsize and secs[2][1] == ACA.itemsize
         self.dgen = np.frombuffer(secs[1][2], DGEN, secs[1][0])
         self.aca = np.frombuffer(secs[2][2], ACA, secs[2][0])
-        self.phases = [Phase(secs[3 + 8 * i: 11 + 8 * i]) for i in range(4)]
+        self.phases = [Phase(secs[3 + 9 * i: 12 + 9 * i]) for i in range(4)]
         self.recompress, self.chol, self.solve, self.lmul = self.phases
 
 
@@ -166,6 +170,17 @@ class Interp:
                     C = tiles[I["t0"]].copy()
                     C[:prod.shape[0], :prod.shape[1]] = I["beta"] * C[:prod.shape[0], :prod.shape[1]] + prod
                     tiles[I["t0"]] = C
+            elif op == VM_MGEMM:          # t0 += sum alpha op(A) op(B), operands straight from the pool
+                C = tiles[I["t0"]].copy()
+                for tm in ph.terms[int(I["goff"]): int(I["goff"]) + int(I["ld"])]:
+                    A = self.gload(int(tm["a_off"]), int(tm["a_ld"]), self.dim(tm["a_rows"]), self.dim(tm["a_cols"]))
+                    B = self.gload(int(tm["b_off"]), int(tm["b_ld"]), self.dim(tm["b_rows"]), self.dim(tm["b_cols"]))
+                    A = A.T if tm["ta"] else A
+                    B = B.T if tm["tb"] else B
+                    k = min(A.shape[1], B.shape[0])
+                    prod = tm["alpha"] * (A[:, :k] @ B[:k, :])
+                    C[:prod.shape[0], :prod.shape[1]] += prod
+                tiles[I["t0"]] = C
             elif op == VM_POTRF:
                 A = tiles[I["t0"]]
                 A = np.tril(A) + np.tril(A, -1).T
