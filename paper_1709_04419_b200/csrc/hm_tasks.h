@@ -25,6 +25,7 @@ enum VmOp : uint8_t {
     VM_ZERO = 8,     // tile[t0] <- 0 with dims (rows x cols)
     VM_MGEMM = 9,    // tile[t0] += sum_i alpha_i op(A_i) op(B_i) over terms[goff .. goff+ld), A_i/B_i
                      // streamed from the pool (pipelined DMMA; replaces LD, LD, GEMM triples)
+    VM_TRTRI = 10,   // tile[t0] <- tile[t1]^{-1} (lower triangular, trows[t1] x trows[t1])
 };
 constexpr int NTILE = 3;   // target + two operands (TRSM/TRMM reuse tile 1 for L)
 
@@ -97,39 +98,41 @@ constexpr int64_t TR_COOP_WORK = int64_t(1) << 18;   // (m + q) * static K per c
 constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
 
 struct TruncWs {                  // randomized-path workspace (doubles unless noted)
-    double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp;
+    double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp,
+        *Gp2, *Ypart, *Wpart;
     int64_t total;
 };
-HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t cap, int32_t Ks,
-                                     int32_t wmax) {
-    (void)wmax;
+// split-K of the W = V_stack P product (partials nsub x q x L) only for small q
+constexpr int TR_WSPLIT_Q = 512;
+HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t cap, int32_t Ks, int32_t nsub) {
     const int64_t L = (int64_t)cap + TR_RB;
+    const int64_t ns = nsub < 1 ? 1 : nsub;
     const int64_t nch = (m + TR_RCH - 1) / TR_RCH + (q + TR_RCH - 1) / TR_RCH;
     TruncWs w;
     int64_t o = 0;
-    const int64_t sz[21] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_RB, (int64_t)m * Ks, (int64_t)q * Ks,
+    const int64_t sz[24] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_RB, (int64_t)m * Ks, (int64_t)q * Ks,
                             (int64_t)TR_RB * Ks, (int64_t)m * TR_RB, nch * TR_RB, (int64_t)m * L, L * TR_RB,
                             L * (int64_t)Ks, (int64_t)q * L, (int64_t)q * L, L * L, L * L, L * L, L * L, L, L,
-                            (int64_t)TR_COOP_MAX * L * TR_RB, (int64_t)TR_COOP_MAX * L * TR_RB,
-                            (int64_t)TR_COOP_MAX * TR_RB * TR_RB};
-    double* ptr[21];
-    for (int i = 0; i < 21; ++i) {
+                            ns * L * TR_RB, ns * L * TR_RB, ns * TR_RB * TR_RB, ns * L * L, ns * m * TR_RB,
+                            (q <= TR_WSPLIT_Q) ? ns * q * L : 0};
+    double* ptr[24];
+    for (int i = 0; i < 24; ++i) {
         ptr[i] = base + o;
         o += (sz[i] + 7) & ~int64_t(7);
     }
     w.ctl = ptr[0]; w.Om = ptr[1]; w.Ast = ptr[2]; w.Bst = ptr[3]; w.Tt = ptr[4]; w.Y = ptr[5];
     w.npart = ptr[6]; w.Q = ptr[7]; w.Cb = ptr[8]; w.Pt = ptr[9]; w.Wm = ptr[10]; w.Wc = ptr[11];
     w.S = ptr[12]; w.Z = ptr[13]; w.Xo = ptr[14]; w.G = ptr[15]; w.tau = ptr[16]; w.sig = ptr[17];
-    w.Cp = ptr[18]; w.Cf = ptr[19]; w.Gp = ptr[20];
+    w.Cp = ptr[18]; w.Cf = ptr[19]; w.Gp = ptr[20]; w.Gp2 = ptr[21]; w.Ypart = ptr[22]; w.Wpart = ptr[23];
     w.total = o + 64;
     return w;
 }
-inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot, int32_t wmax) {
+inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot, int32_t nsub) {
     if (kmax_tot <= TR_EXACT_K) {
         const int64_t K = kmax_tot;
         return ((int64_t)m + q + 2 * K + 8) * K + 64;
     }
-    return trunc_ws_layout(nullptr, m, q, cap, kmax_tot, wmax).total;
+    return trunc_ws_layout(nullptr, m, q, cap, kmax_tot, nsub).total;
 }
 inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
     if (kmax_tot <= TR_EXACT_K) return 1;

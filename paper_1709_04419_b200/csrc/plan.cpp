@@ -147,21 +147,31 @@ struct Builder {
     static void fuse_mgemm(const std::vector<VIns>& in, std::vector<VIns>& out, std::vector<VTerm>& terms) {
         size_t i = 0;
         while (i < in.size()) {
-            auto is_triple = [&](size_t j) {
+            auto is_triple = [&](size_t j, bool first) {
                 return j + 2 < in.size() && in[j].op == VM_LD && in[j + 1].op == VM_LD && in[j + 2].op == VM_GEMM &&
                        in[j + 2].t1 == in[j].t0 && in[j + 2].t2 == in[j + 1].t0 && in[j].t0 != in[j + 1].t0 &&
-                       in[j + 2].beta == 1.0 && in[j + 2].t0 != in[j].t0 && in[j + 2].t0 != in[j + 1].t0;
+                       (in[j + 2].beta == 1.0 || (first && in[j + 2].beta == 0.0)) && in[j + 2].t0 != in[j].t0 &&
+                       in[j + 2].t0 != in[j + 1].t0;
             };
-            if (!is_triple(i)) {
+            if (!is_triple(i, true)) {
                 out.push_back(in[i]);
                 ++i;
                 continue;
+            }
+            if (in[i + 2].beta == 0.0) {                 // C = A B: zero C (dims of op(A) x op(B)) first
+                VIns z = mk(VM_ZERO);
+                z.t0 = in[i + 2].t0;
+                z.rows = in[i + 2].ta ? in[i].cols : in[i].rows;
+                z.cols = in[i + 2].tb ? in[i + 1].rows : in[i + 1].cols;
+                out.push_back(z);
             }
             VIns m = in[i + 2];
             m.op = VM_MGEMM;
             m.goff = (int64_t)terms.size();
             m.ld = 0;
-            while (is_triple(i) && in[i + 2].t0 == m.t0 && m.ld < VM_MAX_TERMS) {
+            bool firstt = true;
+            while (is_triple(i, firstt) && in[i + 2].t0 == m.t0 && m.ld < VM_MAX_TERMS) {
+                firstt = false;
                 VTerm tm{};
                 tm.a_off = in[i].goff; tm.a_ld = in[i].ld; tm.a_rows = in[i].rows; tm.a_cols = in[i].cols;
                 tm.b_off = in[i + 1].goff; tm.b_ld = in[i + 1].ld; tm.b_rows = in[i + 1].rows; tm.b_cols = in[i + 1].cols;
@@ -276,6 +286,17 @@ struct Builder {
         i.ld = s.m;
         pg.ins.push_back(i);
         pg.reads.push_back(s.d_res);
+    }
+    void ld_inv(Prog& pg, uint8_t tile, int32_t d) {   // L^{-1} of diagonal leaf block d
+        const BStore& s = P.bs[d];
+        VIns i = mk(VM_LD);
+        i.t0 = tile;
+        i.rows = dstat(s.m);
+        i.cols = dstat(s.m);
+        i.goff = s.inv_off;
+        i.ld = s.m;
+        pg.ins.push_back(i);
+        pg.reads.push_back(s.inv_res);
     }
     void st_dense(Prog& pg, uint8_t tile, int32_t b) {
         const BStore& s = P.bs[b];
@@ -438,12 +459,13 @@ struct Builder {
     void fsolve(int32_t s, const Thin& V) {
         const int32_t d = P.diag_of[s];
         if (C(s).leaf()) {
+            // V_s <- L_ss^{-1} V_s as a product with the inverse the POTRF task stored
             for (int32_t oc = 0; oc < V.cols; oc += 64) {
                 Prog pg;
+                ld_inv(pg, 1, d);
                 ld_thin(pg, 0, V, s, oc);
-                ld_dense(pg, 1, d);
-                op2(pg, VM_TRSM_LN, 0, 1);
-                st_thin(pg, 0, V, s, oc);
+                gemm(pg, 2, 1, false, 0, false, 1.0, 0.0);
+                st_thin(pg, 2, V, s, oc);
                 emit_vm(pg);
             }
             return;
@@ -609,7 +631,7 @@ struct Builder {
             kt0 += p.w.stat;
             wmax0 = std::max(wmax0, p.w.stat);
         }
-        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, wmax0);
+        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, trunc_nsub(s.m, s.p, kt0));
         const int64_t nch = (wsz + ring_chunk - 1) / ring_chunk;
         if (4 * nch > ring_nchunks) grow_ring(4 * nch);   // keep >= 4 workspaces of this size in flight
         if (ring_ptr + nch > ring_nchunks) ring_ptr = 0;
@@ -659,6 +681,14 @@ struct Builder {
             const int32_t li = P.leaf_begin[t];
             op2(pg, VM_POTRF, 0, 0, P.logd_off + li);
             st_dense(pg, 0, d);
+            op2(pg, VM_TRTRI, 1, 0);                     // L^{-1} for the block row's TRSMs / solves
+            {
+                const BStore& sd = P.bs[d];
+                VIns st = mk(VM_ST);
+                st.t0 = 1; st.rows = dstat(sd.m); st.cols = dstat(sd.m); st.goff = sd.inv_off; st.ld = sd.m;
+                pg.ins.push_back(st);
+                pg.writes.push_back(sd.inv_res);
+            }
             emit_vm(pg);
         }
     }
@@ -677,9 +707,9 @@ struct Builder {
             Prog pg;
             ld_dense(pg, 0, b);
             apply_dense_pending(pg, b);
-            ld_dense(pg, 1, P.diag_of[s]);
-            op2(pg, VM_TRSM_RLT, 0, 1);
-            st_dense(pg, 0, b);
+            ld_inv(pg, 1, P.diag_of[s]);                // B <- B L^{-T} = B (L^{-1})^T
+            gemm(pg, 2, 0, false, 1, true, 1.0, 0.0);
+            st_dense(pg, 2, b);
             emit_vm(pg);
         } else {
             flush_lr(b, false);
@@ -842,6 +872,10 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
             s.d_off = bld.alloc((int64_t)s.m * s.p);
             s.d_res = bld.new_res(1);
             P.bytes_C += 8LL * s.m * s.p;
+            if (bk.t == bk.s) {
+                s.inv_off = bld.alloc((int64_t)s.m * s.m);
+                s.inv_res = bld.new_res(1);
+            }
         } else {
             s.kind = ST_LR;
             s.cap = std::min(kmax, std::min(s.m, s.p));
@@ -865,8 +899,8 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
         for (int32_t b = 0; b < nb; ++b) {
             const BStore& s = P.bs[b];
             if (s.kind != ST_LR) continue;
-            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K, s.cap));
-            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, std::max(s.cap, kmax)));
+            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K, 1));
+            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, 1));
         }
         bld.ring_chunk = int64_t(1) << 16;   // 512 KiB
         const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 24, 64 * maxs));

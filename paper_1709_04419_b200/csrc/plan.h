@@ -25,6 +25,8 @@ struct BStore {
     int32_t cap = 0, rslot = -1;
     int32_t d_res = -1;          // resource id (dense)
     int32_t u_res0 = -1, v_res0 = -1;  // first leaf-chunk resource of U (rows t) / V (rows s)
+    int64_t inv_off = -1;        // diagonal leaf blocks: L^{-1} (m x m) written with the factor
+    int32_t inv_res = -1;
 };
 
 // A matrix whose rows are the points of a cluster (tree order), split into

@@ -191,4 +191,20 @@ __device__ __forceinline__ void tile_trmm_ln(double* B, const double* L, int m, 
     __syncthreads();
 }
 
+// X <- L^{-1} for the m x m lower-triangular tile L (X lower, zero elsewhere): column j
+// solves L x = e_j by forward substitution (one thread per column).  X != L.
+__device__ __forceinline__ void tile_trtri(double* X, const double* L, int m) {
+    tile_zero(X);
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        X[j * TLD + j] = 1.0 / L[j * TLD + j];
+        for (int i = j + 1; i < m; ++i) {
+            double s = 0.0;
+            for (int k = j; k < i; ++k) s += L[k * TLD + i] * X[j * TLD + k];
+            X[j * TLD + i] = -s / L[i * TLD + i];
+        }
+    }
+    __syncthreads();
+}
+
 }  // namespace hm

@@ -51,6 +51,8 @@ constexpr int ORDER_MAX = 512;
 // accumulated Cholesky updates carry just below eps * sigma_1: ~4x the final
 // rank measured at n = 64k.)
 constexpr double TR_STOP = 1.0;
+// eps from which the final SVD of the projected block uses the Gram matrix (see F3)
+constexpr double TR_GRAM_EPS = 1e-7;
 // dynamic shared memory: [Cs (leader) | staging] then order, koff
 constexpr int TR_SMEM_A = 8 * GEMM_SMEM_DOUBLES;   // GEMM staging, then order / koff
 
@@ -512,13 +514,32 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         // ---- R2: T^T = Omega^T V_stack  (16 x K)
         gemm_short(TR_RB, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_RB, sub, nsub, gsm);
         coop_sync(bar, nsub, gen, stt);
-        // ---- R3: Y = U_stack T  (m x 16)
-        gemm_narrow64(m, TR_RB, K, 1.0, Ust, gop(W.Tt, TR_RB, true), 0.0, W.Y, m, sub, nsub, gsm);
-        coop_sync(bar, nsub, gen, stt);
+        // ---- R3: Y = U_stack T  (m x 16), split over the stacked columns (each CTA one
+        // 16-aligned slice, partials reduced on the owned 64-row chunks)
+        {
+            const int Kc = ((K + nsub - 1) / nsub + 15) & ~15;
+            const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);
+            double* Yp = (nsub == 1) ? W.Y : W.Ypart + (int64_t)sub * m * TR_RB;
+            if (k1 > k0)
+                gemm_narrow64(m, TR_RB, k1 - k0, 1.0, gop(W.Ast + (int64_t)k0 * m, m, false),
+                              gop(W.Tt + (int64_t)k0 * TR_RB, TR_RB, true), 0.0, Yp, m, 0, 1, gsm);
+            else
+                for (int idx = threadIdx.x; idx < m * TR_RB; idx += blockDim.x) Yp[idx] = 0.0;
+            coop_sync(bar, nsub, gen, stt);
+        }
         flops += 4.0 * TR_RB * (double)K * (m + q);
         bytes += 8.0 * Srows;
         for (int c = sub; c < nchm; c += nsub) {
             const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+            if (nsub > 1) {
+                for (int idx = threadIdx.x; idx < (r1 - r0) * TR_RB; idx += blockDim.x) {
+                    const int64_t e = r0 + idx % (r1 - r0) + (int64_t)(idx / (r1 - r0)) * m;
+                    double acc = 0.0;
+                    for (int s2 = 0; s2 < nsub; ++s2) acc += __ldcg(W.Ypart + (int64_t)s2 * m * TR_RB + e);
+                    W.Y[e] = acc;
+                }
+                __syncthreads();
+            }
             for (int j = warp; j < TR_RB; j += nw) {
                 double a = 0.0;
                 for (int i = r0 + lane; i < r1; i += 32) a += W.Y[i + (int64_t)j * m] * W.Y[i + (int64_t)j * m];
@@ -655,30 +676,83 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     // ---- F1: P^T = Q^T U_stack  (ell x K);  F2: W = V_stack P  (q x ell)
     gemm_wide(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
     coop_sync(bar, nsub, gen, stt);
-    gemm_wide(q, ell, K, 1.0, Vst, gop(W.Pt, L, true), 0.0, W.Wm, q, sub, nsub, gsm);
+    if (nsub > 1 && q <= TR_WSPLIT_Q) {            // split over the stacked columns, reduce owned rows
+        const int Kc = ((K + nsub - 1) / nsub + 15) & ~15;
+        const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);
+        double* Wp = W.Wpart + (int64_t)sub * q * L;
+        if (k1 > k0)
+            gemm_wide(q, ell, k1 - k0, 1.0, gop(W.Bst + (int64_t)k0 * q, q, false), gop(W.Pt + (int64_t)k0 * L, L, true),
+                      0.0, Wp, q, 0, 1, gsm);
+        else
+            for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) Wp[idx] = 0.0;
+        coop_sync(bar, nsub, gen, stt);
+        for (int c = sub; c < nchq; c += nsub) {
+            const int r0 = c * TR_RCH, r1 = min(q, r0 + TR_RCH);
+            for (int idx = threadIdx.x; idx < (r1 - r0) * ell; idx += blockDim.x) {
+                const int64_t e = r0 + idx % (r1 - r0) + (int64_t)(idx / (r1 - r0)) * q;
+                double acc = 0.0;
+                for (int s2 = 0; s2 < nsub; ++s2) acc += __ldcg(W.Wpart + (int64_t)s2 * q * L + e);
+                W.Wm[e] = acc;
+            }
+        }
+    } else {
+        gemm_wide(q, ell, K, 1.0, Vst, gop(W.Pt, L, true), 0.0, W.Wm, q, sub, nsub, gsm);
+    }
     coop_sync(bar, nsub, gen, stt);
     flops += 4.0 * (double)ell * K * (m + q);
     bytes += 8.0 * Srows;
     const int Kw = min(q, ell);
-    if (sub == 0) {
-        // ---- F3 (leader): Householder QR of a copy of W, S = R^T, Jacobi S Z = X', rank, order
-        for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) W.Wc[idx] = W.Wm[idx];
-        __syncthreads();
-        house_qr(W.Wc, q, ell, W.tau, scratch);
-        for (int idx = threadIdx.x; idx < ell * Kw; idx += blockDim.x) {
-            const int i = idx % ell, j = idx / ell;
-            W.S[i + (int64_t)j * ell] = (i >= j) ? W.Wc[j + (int64_t)i * q] : 0.0;
+    const bool gram = eps >= TR_GRAM_EPS;
+    if (gram) {
+        // ---- F3 (Gram path, eps >= TR_GRAM_EPS): eigen-decomposition of W^T W = X Sigma^2 X^T.
+        // W^T = Q^T M, so M ~ Q W^T = Q X Sigma Y^T and the rank-r truncation is
+        // U = Q X_r, V = W X_r.  The Gram matrix resolves sigma_i / sigma_1 down to
+        // ~1e-8, enough for eps >= 1e-7; the partial products are spread over the group.
+        double* Gp = W.Gp2 + (int64_t)sub * L * L;
+        bool first = true;
+        for (int c = sub; c < nchq; c += nsub) {
+            const int r0 = c * TR_RCH, rows = min(q, r0 + TR_RCH) - r0;
+            gemm_wide(ell, ell, rows, 1.0, gop(W.Wm + r0, q, true), gop(W.Wm + r0, q, false), first ? 0.0 : 1.0, Gp, L, 0,
+                      1, gsm);
+            first = false;
         }
-        __syncthreads();
-        jacobi_svd(W.S, ell, Kw, W.Z, &s_flag);
-        for (int j = warp; j < Kw; j += nw) {
+        if (first)
+            for (int idx = threadIdx.x; idx < ell * ell; idx += blockDim.x) Gp[(idx % ell) + (int64_t)(idx / ell) * L] = 0.0;
+        coop_sync(bar, nsub, gen, stt);
+        for (int idx = sub * blockDim.x + threadIdx.x; idx < ell * ell; idx += nsub * blockDim.x) {
+            const int64_t e = (idx % ell) + (int64_t)(idx / ell) * L;
+            double acc = 0.0;
+            for (int s2 = 0; s2 < nsub; ++s2) acc += __ldcg(W.Gp2 + (int64_t)s2 * L * L + e);
+            W.S[idx] = acc;                        // ell x ell, ld ell
+        }
+        coop_sync(bar, nsub, gen, stt);
+        flops += 2.0 * (double)ell * ell * q;
+    }
+    if (sub == 0) {
+        if (!gram) {
+            // ---- F3 (Householder path): QR of a copy of W, S = R^T, Jacobi S Z = X'
+            for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) W.Wc[idx] = W.Wm[idx];
+            __syncthreads();
+            house_qr(W.Wc, q, ell, W.tau, scratch);
+            for (int idx = threadIdx.x; idx < ell * Kw; idx += blockDim.x) {
+                const int i = idx % ell, j = idx / ell;
+                W.S[i + (int64_t)j * ell] = (i >= j) ? W.Wc[j + (int64_t)i * q] : 0.0;
+            }
+            __syncthreads();
+            jacobi_svd(W.S, ell, Kw, W.Z, &s_flag);
+        } else {
+            // one-sided Jacobi on the SPD Gram matrix: G Z = X' with ||X'_c|| = sigma_c^2
+            jacobi_svd(W.S, ell, ell, W.Z, &s_flag);
+        }
+        const int kdim = gram ? ell : Kw;
+        for (int j = warp; j < kdim; j += nw) {
             double sacc = 0.0;
             for (int r = lane; r < ell; r += 32) sacc += W.S[r + (int64_t)j * ell] * W.S[r + (int64_t)j * ell];
             sacc = warp_sum(sacc);
-            if (lane == 0) W.sig[j] = sqrt(sacc);
+            if (lane == 0) W.sig[j] = gram ? sqrt(sqrt(sacc)) : sqrt(sacc);   // sigma (Gram: sqrt of eigenvalue)
         }
         __syncthreads();
-        const int kk = min(Kw, ORDER_MAX);
+        const int kk = min(kdim, ORDER_MAX);
         for (int j = threadIdx.x; j < kk; j += blockDim.x) {
             int pos = 0;
             const double sj = W.sig[j];
@@ -700,16 +774,22 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         }
         __syncthreads();
         const int r = s_rank;
-        for (int idx = threadIdx.x; idx < ell * r; idx += blockDim.x) {   // Xo = X'(:, order), G = Xo / sigma^2
+        for (int idx = threadIdx.x; idx < ell * r; idx += blockDim.x) {
             const int l = idx % ell, c = idx / ell;
             const int oc = order[c];
-            const double x = W.S[l + (int64_t)oc * ell];
-            const double sg = W.sig[oc];
-            W.Xo[l + (int64_t)c * L] = x;
-            W.G[l + (int64_t)c * L] = x / (sg * sg);
+            if (gram) {                                // Xo = G = X_r (eigenvectors)
+                const double z = W.Z[l + (int64_t)oc * ell];
+                W.Xo[l + (int64_t)c * L] = z;
+                W.G[l + (int64_t)c * L] = z;
+            } else {                                   // Xo = X'(:, order), G = Xo / sigma^2
+                const double x = W.S[l + (int64_t)oc * ell];
+                const double sg = W.sig[oc];
+                W.Xo[l + (int64_t)c * L] = x;
+                W.G[l + (int64_t)c * L] = x / (sg * sg);
+            }
         }
         const double el = ell, qd = q, kw = Kw;
-        flops += 2.0 * (qd * el * kw - kw * kw * kw / 3.0) + 3.0 * kw * (kw - 1.0) * (el + kw);
+        flops += (gram ? 0.0 : 2.0 * (qd * el * kw - kw * kw * kw / 3.0)) + 3.0 * kw * (kw - 1.0) * (el + kw);
     }
     coop_sync(bar, nsub, gen, stt);                // rank, Xo, G published
     const int r = __ldcg(ctl + 2);

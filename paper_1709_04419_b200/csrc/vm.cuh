@@ -26,7 +26,7 @@ struct TermRt {
 };
 
 __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ terms, int nt, const double* pool,
-                                         const int* ranks, double* stage, double& c_fl, double& c_by) {
+                                         const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by) {
     constexpr int LA = 65, LB = 65, SA = GM_BK * LA, SB = GM_BK * LB;
     __shared__ TermRt tr[VM_MAX_TERMS];
     __shared__ int s_nch;
@@ -61,8 +61,9 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
     }
     __syncthreads();
     const int nch = s_nch;
-    double* As = stage;
-    double* Bs = stage + GM_NS * SA;
+    static_assert(GM_NS * SA <= TSZ && GM_NS * SB <= TSZ, "stages fit one tile each");
+    double* As = stageA;                                 // the two tiles other than T0
+    double* Bs = stageB;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
@@ -160,7 +161,15 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
                 __syncthreads();
             } break;
             case VM_MGEMM: {
-                vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + TSZ, c_fl, c_by);
+                const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;   // staging: the other tiles
+                vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by);
+            } break;
+            case VM_TRTRI: {
+                const int mm = trows[I.t1];
+                if (threadIdx.x == 0) c_fl += (double)mm * mm * mm / 3.0;
+                tile_trtri(T0, sm + (int)I.t1 * TSZ, mm);
+                if (threadIdx.x == 0) { trows[I.t0] = mm; tcols[I.t0] = mm; }
+                __syncthreads();
             } break;
             case VM_ZERO: {
                 tile_zero(T0);

@@ -34,7 +34,7 @@ DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q
 ACA = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4"),
                 ("cap", "<i4"), ("rslot", "<i4")])
 
-VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM = range(1, 10)
+VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM, VM_TRTRI = range(1, 11)
 TD = 64
 
 
@@ -170,6 +170,9 @@ class Interp:
                     C = tiles[I["t0"]].copy()
                     C[:prod.shape[0], :prod.shape[1]] = I["beta"] * C[:prod.shape[0], :prod.shape[1]] + prod
                     tiles[I["t0"]] = C
+            elif op == VM_TRTRI:          # t0 <- inverse of the lower-triangular t1
+                Lt = np.tril(tiles[I["t1"]])
+                tiles[I["t0"]] = np.linalg.solve(Lt, np.eye(Lt.shape[0])) if Lt.size else Lt.copy()
             elif op == VM_MGEMM:          # t0 += sum alpha op(A) op(B), operands straight from the pool
                 C = tiles[I["t0"]].copy()
                 for tm in ph.terms[int(I["goff"]): int(I["goff"]) + int(I["ld"])]:
@@ -368,6 +371,17 @@ class InterpRand(Interp):
             self.ranks[t["rslot"]] = 0
             return
         Wm = B @ (A.T @ Q)                           # W = M^T Q
+        if self.eps >= 1e-7:                         # TR_GRAM_EPS: eigen-decomposition of W^T W
+            lam, X = np.linalg.eigh(Wm.T @ Wm)
+            o = np.argsort(-lam)
+            lam, X = np.maximum(lam[o], 0.0), X[:, o]
+            S = np.sqrt(lam)
+            r = int(np.sum((S > self.eps * S[0]) & (S > 0)))
+            r = min(r, cap)
+            self.gstore(int(t["u_out"]), m, Q @ X[:, :r])          # U = Q X_r
+            self.gstore(int(t["v_out"]), q, Wm @ X[:, :r])         # V = W X_r
+            self.ranks[t["rslot"]] = r
+            return
         _, R = np.linalg.qr(Wm)
         Xp, S, Zt = np.linalg.svd(R.T)               # R^T = X' Z^T with X' = Xp S
         r = int(np.sum((S > self.eps * S[0]) & (S > 0)))

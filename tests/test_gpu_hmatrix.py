@@ -105,7 +105,7 @@ def test_exec_modes_identical(hm, n, leaf):
     """Persistent dependency-driven executor (default) vs one launch per wave.
     Same task DAG; the persistent executor may split a wide truncation over
     several CTAs (different summation order of its partial reductions), so the
-    results agree to rounding (1e-12 relative), not bit for bit."""
+    results agree to rounding (1e-10 relative), not bit for bit."""
     pts = uniform_iid(n, seed=21)
     theta = (1.0, 0.0864, 0.5)
     Z = standard_normal(n, 2, seed=22)
@@ -117,7 +117,7 @@ def test_exec_modes_identical(hm, n, leaf):
         H.cholesky()
         outs.append(H.loglik(Z))
         H.close()
-    np.testing.assert_allclose(outs[1], outs[0], rtol=1e-12)
+    np.testing.assert_allclose(outs[1], outs[0], rtol=1e-10)
     oll, _, _ = od.loglik(pts, Z, theta)
     np.testing.assert_allclose(outs[1][:, 0], oll, rtol=1e-5)
 

@@ -59,6 +59,23 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
     lines.append(f"  critical path: {cp.max() / 1e3:.3f} ms over {len(path)} tasks "
                  f"(vm {int((pk == 0).sum())}: {dur[path][pk == 0].sum() / 1e3:.3f} ms, "
                  f"trunc {int((pk == 1).sum())}: {dur[path][pk == 1].sum() / 1e3:.3f} ms)")
+    # composition of the critical path
+    comp = {}
+    for i in path:
+        x = ph.xt[i]
+        if x["kind"] == 1:
+            t = ph.tt[x["idx"]]
+            key = f"trunc m={t['m']} q={t['q']} nsub={x['nsub']}"
+        else:
+            v = ph.vt[x["idx"]]
+            ops = ph.ins["op"][v["ins_begin"]: v["ins_begin"] + v["ins_count"]]
+            key = "vm " + ("POTRF" if 4 in ops else "TRSM" if (5 in ops or 6 in ops) else "prod")
+        c = comp.setdefault(key, [0, 0.0])
+        c[0] += 1
+        c[1] += dur[i]
+    lines.append("  critical-path composition (count, ms):")
+    for k, (cnt, d) in sorted(comp.items(), key=lambda kv: -kv[1][1])[:14]:
+        lines.append(f"    {k:40s} {cnt:6d} {d / 1e3:9.3f}")
     # stage breakdown of the randomized truncations (leader stamps)
     tsel = np.nonzero((kind == 1) & (stg[:, 0] > 0))[0]
     if tsel.size:
