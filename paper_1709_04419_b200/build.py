@@ -20,9 +20,10 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+EXTRA = os.environ.get("HM_BUILD_DEFS", "").split()   # debug / experiment -D flags
+NVCC_FLAGS = [*EXTRA, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", INCLUDE]
-CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I", INCLUDE,
+CXX_FLAGS = [*EXTRA, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-I", INCLUDE,
              "-I", os.path.join(CUDA, "include")]
 
 

@@ -94,7 +94,10 @@ constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
 constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
 constexpr int TR_TCH = 128;       // stacked columns staged per shared-memory chunk
 constexpr int TR_PMAX = 1023;     // pieces per truncation
-constexpr int64_t TR_COOP_WORK = int64_t(1) << 18;   // (m + q) * static K per cooperating CTA
+#ifndef HM_COOP_WORK_LOG2
+#define HM_COOP_WORK_LOG2 18
+#endif
+constexpr int64_t TR_COOP_WORK = int64_t(1) << HM_COOP_WORK_LOG2;   // (m + q) * static K per cooperating CTA
 constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
 
 struct TruncWs {                  // randomized-path workspace (doubles unless noted)

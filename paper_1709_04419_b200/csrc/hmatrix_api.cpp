@@ -10,6 +10,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -51,6 +52,7 @@ struct hm_handle_s {
     int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
     DevBuf trace;        // per-task timestamps of the last executor launch (hm_trace)
     bool tracing = false;
+    bool poison = false;   // HM_POISON_RING: NaN-fill the workspace ring before every phase (tests)
     int64_t trace_n = 0;
     // profiling: per kernel family (KF_*) launch counts (always) and, when
     // enabled, a CUDA event pair around every launch on the handle's stream
@@ -117,6 +119,8 @@ struct Launch {
 
 void run_phase(hm_handle_s* h, const DPhase& d) {
     const Phase& p = *d.ph;
+    if (h->poison)   // diagnostics (HM_POISON_RING=1): NaN-fill the truncation workspaces first
+        HM_CUDA_TRY(cudaMemsetAsync(h->pool.as<double>() + h->P.ring_off, 0xFF, sizeof(double) * h->P.ring_size, h->stream));
     double* pool = h->pool.as<double>();
     int* ranks = h->ranks.as<int>();
     int* flags = h->flags.as<int>();
@@ -274,6 +278,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         h = new hm_handle_s();
         h->device = device;
         h->prm = params;
+        if (const char* pz = std::getenv("HM_POISON_RING")) h->poison = pz[0] == '1';
         if (stream) {
             h->stream = (cudaStream_t)stream;
         } else {

@@ -53,6 +53,7 @@ constexpr int ORDER_MAX = 512;
 constexpr double TR_STOP = 1.0;
 // eps from which the final SVD of the projected block uses the Gram matrix (see F3)
 constexpr double TR_GRAM_EPS = 1e-7;
+
 // dynamic shared memory: [Cs (leader) | staging] then order, koff
 constexpr int TR_SMEM_A = 8 * GEMM_SMEM_DOUBLES;   // GEMM staging, then order / koff
 
@@ -426,7 +427,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     const int Ks = t.kmax_tot;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nchm = (m + TR_RCH - 1) / TR_RCH, nchq = (q + TR_RCH - 1) / TR_RCH;
-    TruncWs W = trunc_ws_layout(pool + t.ws, m, q, cap, Ks, t.wmax);
+    TruncWs W = trunc_ws_layout(pool + t.ws, m, q, cap, Ks, t.nsub);
     int* ctl = (int*)W.ctl;                        // [0] done, [1] ell, [2] rank, [3] added, [8..] order
     double* gsm = dsm;                             // GEMM staging
     int* koff = (int*)((char*)dsm + TR_SMEM_A + ORDER_MAX * 4);   // TR_PMAX + 1 ints

@@ -139,3 +139,21 @@ def test_repeat_evaluations_bit_identical(hm):
     for s, o in zip(sums[1:], outs[1:]):
         assert np.array_equal(s, sums[0])
         assert np.array_equal(o, outs[0])
+
+
+def test_no_uninitialised_workspace_reads(hm, monkeypatch):
+    """Every truncation workspace is written before it is read: with the
+    workspace ring NaN-filled before every phase (HM_POISON_RING=1) the results
+    are bit-identical (this caught a host/device workspace-layout mismatch)."""
+    pts = uniform_iid(2000, seed=11)
+    theta = (1.0, 0.0864, 0.5)
+    Z = standard_normal(2000, 1, seed=5)
+    outs = []
+    for poison in ("0", "1"):
+        monkeypatch.setenv("HM_POISON_RING", poison)
+        H = hm.HMatrix(pts, theta, eps=1e-7, leaf=32, eta=2.0)
+        H.cholesky()
+        outs.append(H.loglik(Z))
+        H.close()
+    assert np.all(np.isfinite(outs[1]))
+    assert np.array_equal(outs[0], outs[1])

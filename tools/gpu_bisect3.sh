@@ -1,0 +1,3 @@
+rm -rf paper_1709_04419_b200/build paper_1709_04419_b200/lib
+HM_BUILD_DEFS="-DHM_WS_SLACK=262144" python paper_1709_04419_b200/build.py > /dev/null
+timeout 120 python tools/hm_probe3.py 2000 1e-8 2>&1 | head -3
