@@ -21,7 +21,7 @@
 namespace hm {
 
 constexpr int GM_BK = 16;
-constexpr int GM_NS = 3;
+constexpr int GM_NS = 4;
 
 struct GOp {
     const double* p;

@@ -26,7 +26,9 @@ enum VmOp : uint8_t {
     VM_MGEMM = 9,    // tile[t0] += sum_i alpha_i op(A_i) op(B_i) over terms[goff .. goff+ld), A_i/B_i
                      // streamed from the pool (pipelined DMMA; replaces LD, LD, GEMM triples)
     VM_TRTRI = 10,   // tile[t0] <- tile[t1]^{-1} (lower triangular, trows[t1] x trows[t1])
+    VM_ADD = 11,     // tile[t0] += tile[t1]
 };
+constexpr int VM_PARTIAL_TERMS = 8;   // dense-update terms per independent partial-sum task
 constexpr int NTILE = 3;   // target + two operands (TRSM/TRMM reuse tile 1 for L)
 
 // Dimension spec: actual = (slot < 0) ? stat : clamp(ranks[slot] - off, 0, stat)
@@ -89,13 +91,15 @@ struct TTask {
 
 // k_trunc algorithm selection and workspace (trunc.cuh; planner sizes the workspace)
 constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs
-constexpr int TR_RB = 16;         // probes per round of the randomized range finder
+constexpr int TR_RB = 16;         // probes per block of the randomized range finder
+constexpr int TR_NB = 3;          // blocks per pass over the stacks
+constexpr int TR_PW = TR_RB * TR_NB;
 constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
 constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
 constexpr int TR_TCH = 128;       // stacked columns staged per shared-memory chunk
 constexpr int TR_PMAX = 1023;     // pieces per truncation
 #ifndef HM_COOP_WORK_LOG2
-#define HM_COOP_WORK_LOG2 18
+#define HM_COOP_WORK_LOG2 17
 #endif
 constexpr int64_t TR_COOP_WORK = int64_t(1) << HM_COOP_WORK_LOG2;   // (m + q) * static K per cooperating CTA
 constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
@@ -113,10 +117,10 @@ HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t
     const int64_t nch = (m + TR_RCH - 1) / TR_RCH + (q + TR_RCH - 1) / TR_RCH;
     TruncWs w;
     int64_t o = 0;
-    const int64_t sz[24] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_RB, (int64_t)m * Ks, (int64_t)q * Ks,
-                            (int64_t)TR_RB * Ks, (int64_t)m * TR_RB, nch * TR_RB, (int64_t)m * L, L * TR_RB,
+    const int64_t sz[24] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_PW, (int64_t)m * Ks, (int64_t)q * Ks,
+                            (int64_t)TR_PW * Ks, (int64_t)m * TR_PW, nch * TR_PW, (int64_t)m * L, L * TR_RB,
                             L * (int64_t)Ks, (int64_t)q * L, (int64_t)q * L, L * L, L * L, L * L, L * L, L, L,
-                            ns * L * TR_RB, ns * L * TR_RB, ns * TR_RB * TR_RB, ns * L * L, ns * m * TR_RB,
+                            ns * L * TR_RB, ns * L * TR_RB, ns * TR_RB * TR_RB, ns * L * L, ns * m * TR_PW,
                             (q <= TR_WSPLIT_Q) ? ns * q * L : 0};
     double* ptr[24];
     for (int i = 0; i < 24; ++i) {
@@ -139,8 +143,16 @@ inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot
 }
 inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
     if (kmax_tot <= TR_EXACT_K) return 1;
+    // one CTA per TR_COOP_WORK of stacked data, at most two per 64-row chunk of the
+    // larger side (a group must assemble before it starts: more CTAs than rows to
+    // share only adds waiting), at most TR_COOP_MAX
     const int64_t g = ((int64_t)(m + q) * kmax_tot) / TR_COOP_WORK;
-    return (int32_t)(g < 1 ? 1 : (g > TR_COOP_MAX ? TR_COOP_MAX : g));
+    const int64_t rows = (m > q ? m : q);
+    const int64_t gmax = 2 * ((rows + TR_RCH - 1) / TR_RCH);
+    int64_t n = g < 1 ? 1 : g;
+    if (n > gmax) n = gmax;
+    if (n > TR_COOP_MAX) n = TR_COOP_MAX;
+    return (int32_t)n;
 }
 
 // ---- dependency-driven execution (persistent executor, exec.cu) --------

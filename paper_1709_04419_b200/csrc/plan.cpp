@@ -545,24 +545,71 @@ struct Builder {
     }
 
     // dense leaf target: t0 holds B; apply pending products and pieces
+    // dense leaf target: t0 holds B; apply pending products and pieces.  Long update
+    // lists are split: every VM_PARTIAL_TERMS terms form an independent task that
+    // accumulates its partial sum into a temporary tile (ring of 64 x 64 slots) as
+    // soon as its own operands exist; the target's task then only adds the partials.
+    // This moves the bulk of the update off the Cholesky's critical path.
     void apply_dense_pending(Prog& pg, int32_t b) {
         Pend pd = std::move(pend[b]);
         pend[b] = Pend();
+        std::vector<Prog> terms;
         for (auto& pr : pd.prods) {
             const int32_t X = pr.first, Y = pr.second;
             if (P.bs[X].kind != ST_DENSE || P.bs[Y].kind != ST_DENSE)
                 throw std::logic_error("leaf product with non-dense factor");
-            ld_dense(pg, 1, X);
-            ld_dense(pg, 2, Y);
-            gemm(pg, 0, 1, false, 2, true, -1.0, 1.0);
+            Prog t;
+            ld_dense(t, 1, X);
+            ld_dense(t, 2, Y);
+            gemm(t, 0, 1, false, 2, true, -1.0, 1.0);
+            terms.push_back(std::move(t));
         }
         for (auto& pc : pd.pieces) {
             for (int32_t kc = 0; kc < pc.U.cols; kc += 64) {
-                ld_thin(pg, 1, pc.U, pc.U.cluster, kc);
-                ld_thin(pg, 2, pc.V, pc.V.cluster, kc);
-                gemm(pg, 0, 1, false, 2, true, pc.alpha, 1.0);
+                Prog t;
+                ld_thin(t, 1, pc.U, pc.U.cluster, kc);
+                ld_thin(t, 2, pc.V, pc.V.cluster, kc);
+                gemm(t, 0, 1, false, 2, true, pc.alpha, 1.0);
+                terms.push_back(std::move(t));
             }
         }
+        auto append = [](Prog& dst, const Prog& src) {
+            dst.ins.insert(dst.ins.end(), src.ins.begin(), src.ins.end());
+            dst.reads.insert(dst.reads.end(), src.reads.begin(), src.reads.end());
+            dst.writes.insert(dst.writes.end(), src.writes.begin(), src.writes.end());
+        };
+        if ((int)terms.size() <= VM_PARTIAL_TERMS) {
+            for (auto& t : terms) append(pg, t);
+            return;
+        }
+        const BStore& st = P.bs[b];
+        for (size_t c0 = 0; c0 < terms.size(); c0 += VM_PARTIAL_TERMS) {
+            Prog pt;
+            zero(pt, 0, dstat(st.m), dstat(st.p));
+            for (size_t i = c0; i < std::min(terms.size(), c0 + VM_PARTIAL_TERMS); ++i) append(pt, terms[i]);
+            const int64_t slot = tmp_alloc(pt.writes);
+            VIns sti = mk(VM_ST);
+            sti.t0 = 0; sti.rows = dstat(st.m); sti.cols = dstat(st.p); sti.goff = slot; sti.ld = st.m;
+            pt.ins.push_back(sti);
+            emit_vm(pt);
+            VIns ld = mk(VM_LD);
+            ld.t0 = 1; ld.rows = dstat(st.m); ld.cols = dstat(st.p); ld.goff = slot; ld.ld = st.m;
+            pg.ins.push_back(ld);
+            pg.reads.push_back(tmp_res[(slot - P.tmp_off) / TMP_SLOT]);
+            op2(pg, VM_ADD, 0, 1);
+        }
+    }
+
+    // temporary-tile ring for the partial sums (slots of TMP_SLOT doubles; each slot
+    // is a dependency resource, so a slot is reused only after its reader ran)
+    static constexpr int64_t TMP_SLOT = 64 * 64;
+    std::vector<int32_t> tmp_res;
+    int64_t tmp_ptr = 0;
+    int64_t tmp_alloc(std::vector<int32_t>& writes) {
+        const int64_t s = tmp_ptr;
+        tmp_ptr = (tmp_ptr + 1) % (int64_t)tmp_res.size();
+        writes.push_back(tmp_res[s]);
+        return P.tmp_off + s * TMP_SLOT;
     }
 
     // evaluate product X Y^T into truncation pieces placed at (row0, col0) of the target
@@ -725,6 +772,7 @@ struct Builder {
         traw.clear();
         xraw.clear();
         ring_ptr = 0;
+        tmp_ptr = 0;
         std::fill(lw_wave.begin(), lw_wave.end(), -1);
         std::fill(rd_wave.begin(), rd_wave.end(), -1);
         std::fill(lw_task.begin(), lw_task.end(), -1);
@@ -892,6 +940,12 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     P.z_off = bld.alloc((int64_t)T.n * P.zw);
     const int32_t z_res0 = bld.new_res(P.n_leaves);
     P.pool_blocks = bld.bump;
+    // temporary 64 x 64 tiles for split dense updates (see apply_dense_pending)
+    {
+        const int64_t nslots = 8192;   // 256 MiB
+        P.tmp_off = bld.alloc(nslots * Builder::TMP_SLOT);
+        for (int64_t i = 0; i < nslots; ++i) bld.tmp_res.push_back(bld.new_res(1));
+    }
     // truncation workspace ring: starts at >= 4x the largest recompression workspace
     // (min 128 MiB) and grows to >= 4x the largest workspace the Cholesky emits
     {

@@ -72,6 +72,7 @@ struct Plan {
     int32_t zw = 64;
     int64_t bytes_C = 0;               // bytes of block storage at capacity
     int64_t ring_off = 0, ring_size = 0;  // truncation workspace ring (doubles)
+    int64_t tmp_off = 0;                  // ring of 64 x 64 temporary tiles (split dense updates)
     // assembly
     std::vector<DenseGenTask> dgen;
     std::vector<AcaTask> aca;

@@ -191,6 +191,12 @@ __device__ __forceinline__ void tile_trmm_ln(double* B, const double* L, int m, 
     __syncthreads();
 }
 
+// A += B over the whole tile (both zero outside their logical dims)
+__device__ __forceinline__ void tile_add(double* A, const double* B) {
+    for (int i = threadIdx.x; i < TSZ; i += blockDim.x) A[i] += B[i];
+    __syncthreads();
+}
+
 // X <- L^{-1} for the m x m lower-triangular tile L (X lower, zero elsewhere): column j
 // solves L x = e_j by forward substitution (one thread per column).  X != L.
 __device__ __forceinline__ void tile_trtri(double* X, const double* L, int m) {

@@ -164,6 +164,10 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
                 const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;   // staging: the other tiles
                 vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by);
             } break;
+            case VM_ADD: {
+                if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * tcols[I.t0];
+                tile_add(T0, sm + (int)I.t1 * TSZ);
+            } break;
             case VM_TRTRI: {
                 const int mm = trows[I.t1];
                 if (threadIdx.x == 0) c_fl += (double)mm * mm * mm / 3.0;

@@ -34,7 +34,7 @@ DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q
 ACA = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4"),
                 ("cap", "<i4"), ("rslot", "<i4")])
 
-VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM, VM_TRTRI = range(1, 11)
+VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM, VM_TRTRI, VM_ADD = range(1, 12)
 TD = 64
 
 
@@ -170,6 +170,11 @@ class Interp:
                     C = tiles[I["t0"]].copy()
                     C[:prod.shape[0], :prod.shape[1]] = I["beta"] * C[:prod.shape[0], :prod.shape[1]] + prod
                     tiles[I["t0"]] = C
+            elif op == VM_ADD:            # t0 += t1 (same logical dims)
+                A = tiles[I["t0"]].copy()
+                B = tiles[I["t1"]]
+                A[:B.shape[0], :B.shape[1]] += B
+                tiles[I["t0"]] = A
             elif op == VM_TRTRI:          # t0 <- inverse of the lower-triangular t1
                 Lt = np.tril(tiles[I["t1"]])
                 tiles[I["t0"]] = np.linalg.solve(Lt, np.eye(Lt.shape[0])) if Lt.size else Lt.copy()
@@ -330,7 +335,7 @@ class InterpRand(Interp):
             Om = self.rng.standard_normal((q, self.RB))
             Y = A @ (B.T @ Om)
             sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0))))   # ~ ||M||_F
-            thr = self.eps * sest * 1.0          # TR_STOP: relative Frobenius certificate
+            thr = self.eps * sest * 4.0          # TR_STOP: relative Frobenius certificate
             for _ in range(2):                       # BCGS2, first projection (twice)
                 Y = Y - Q @ (Q.T @ Y)
             G = Y.T @ Y                              # pivoted Cholesky-QR of the block
@@ -371,15 +376,41 @@ class InterpRand(Interp):
             self.ranks[t["rslot"]] = 0
             return
         Wm = B @ (A.T @ Q)                           # W = M^T Q
-        if self.eps >= 1e-7:                         # TR_GRAM_EPS: eigen-decomposition of W^T W
-            lam, X = np.linalg.eigh(Wm.T @ Wm)
-            o = np.argsort(-lam)
-            lam, X = np.maximum(lam[o], 0.0), X[:, o]
-            S = np.sqrt(lam)
-            r = int(np.sum((S > self.eps * S[0]) & (S > 0)))
-            r = min(r, cap)
-            self.gstore(int(t["u_out"]), m, Q @ X[:, :r])          # U = Q X_r
-            self.gstore(int(t["v_out"]), q, Wm @ X[:, :r])         # V = W X_r
+        if self.eps >= 1e-7:                         # TR_GRAM_EPS: pivoted Cholesky of W^T W
+            G = Wm.T @ Wm
+            ell = G.shape[0]
+            cut = self.eps ** 2 * float(np.max(np.diag(G)))
+            piv = list(range(ell))
+            R = np.zeros((ell, ell))
+            r = 0
+            for k in range(ell):
+                jb = k + int(np.argmax([G[piv[j], piv[j]] for j in range(k, ell)]))
+                piv[k], piv[jb] = piv[jb], piv[k]
+                d = G[piv[k], piv[k]]
+                if not d > cut:
+                    break
+                if k >= cap:
+                    break
+                R[k, k] = math.sqrt(d)
+                for j in range(k + 1, ell):
+                    R[k, j] = G[piv[k], piv[j]] / R[k, k]
+                for i in range(k + 1, ell):
+                    for j in range(i, ell):
+                        v = G[piv[i], piv[j]] - R[k, i] * R[k, j]
+                        G[piv[i], piv[j]] = v
+                        G[piv[j], piv[i]] = v
+                r = k + 1
+            Xo = np.zeros((ell, r))
+            Gm = np.zeros((ell, r))
+            Rinv = np.linalg.inv(np.triu(R[:r, :r])) if r else np.zeros((0, 0))
+            for c in range(r):
+                for j in range(ell):
+                    if j >= c:
+                        Xo[piv[j], c] = R[c, j]
+                for j in range(c + 1):
+                    Gm[piv[j], c] = Rinv[j, c]
+            self.gstore(int(t["u_out"]), m, Q @ Xo)                # U = Q P R^T
+            self.gstore(int(t["v_out"]), q, Wm @ Gm)               # V = W P_r R11^-1
             self.ranks[t["rslot"]] = r
             return
         _, R = np.linalg.qr(Wm)

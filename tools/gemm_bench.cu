@@ -16,6 +16,7 @@ __global__ void kgemm(int M, int N, int K, const double* A, int lda, bool tA, co
         if (SHAPE == 0) gemm_wide(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
         if (SHAPE == 1) gemm_narrow(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
         if (SHAPE == 2) gemm_short(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
+        if (SHAPE == 3) gemm_narrow64(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
     }
 }
 __global__ void kref(int M, int N, int K, const double* A, int lda, bool tA, const double* B, int ldb, bool tB, double* C,
@@ -59,6 +60,8 @@ void run(const char* name, int M, int N, int K, bool tA, bool tB, int grid) {
 }
 int main() {
     run<1>("narrow", 256, 16, 1700, false, true, 1);      // R3: Y = Ast T
+    run<3>("narrow64", 128, 16, 1500, false, true, 1);    // R3 small
+    run<2>("short", 16, 1500, 128, true, false, 1);       // R2 small
     run<2>("short", 16, 1700, 256, true, false, 1);       // R2: T^T = Om^T Bst
     run<0>("wide", 48, 1700, 256, true, false, 1);        // F1: P^T = Q^T Ast
     run<0>("wide", 256, 48, 1700, false, true, 1);        // F2: W = Bst P

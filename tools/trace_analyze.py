@@ -80,14 +80,16 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
     tsel = np.nonzero((kind == 1) & (stg[:, 0] > 0))[0]
     if tsel.size:
         lines.append("  randomized truncation stages (leader), us: [start->sync1, sync1->sync2, ...]")
-        single = tsel[ph.xt["nsub"][tsel] == 1]
-        pick = list(tsel[np.argsort(-dur[tsel])][:6]) + list(single[np.argsort(-dur[single])][:6])
+        mid = np.array([i for i in tsel if ph.tt[ph.xt[i]["idx"]]["m"] <= 512], dtype=np.int64)
+        pick = list(tsel[np.argsort(-dur[tsel])][:3]) + (list(mid[np.argsort(-dur[mid])][:6]) if mid.size else [])
         for i in pick:
-            st = stg[i]
+            st = stg[i].copy()
+            Kc, ellc = int(st[62]), int(st[63])
+            st[62] = st[63] = 0
             k = int(np.max(np.nonzero(st)[0]))
             d = np.diff(st[:k + 1].astype(np.float64)) * 1e-3
             x = ph.xt[i]; t = ph.tt[x["idx"]]
-            lines.append(f"    m={t['m']} q={t['q']} nsub={x['nsub']} total={dur[i]:.0f}: " + " ".join(f"{v:.0f}" for v in d))
+            lines.append(f"    m={t['m']} q={t['q']} nsub={x['nsub']} K={Kc} ell={ellc} total={dur[i]:.0f}: " + " ".join(f"{v:.0f}" for v in d))
     order = np.argsort(-dur)[:top]
     lines.append("  longest tasks:")
     for i in order:
