@@ -69,7 +69,16 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
         else:
             v = ph.vt[x["idx"]]
             ops = ph.ins["op"][v["ins_begin"]: v["ins_begin"] + v["ins_count"]]
-            key = "vm " + ("POTRF" if 4 in ops else "TRSM" if (5 in ops or 6 in ops) else "prod")
+            names = {1: "LD", 2: "ST", 3: "GEMM", 4: "POTRF", 5: "TRSM", 6: "TRSMLN", 7: "TRMM", 8: "ZERO", 9: "MG",
+                     10: "TRTRI", 11: "ADD"}
+            sig = []
+            for o in ops:
+                nm = names.get(int(o), str(int(o)))
+                if not sig or sig[-1][0] != nm:
+                    sig.append([nm, 1])
+                else:
+                    sig[-1][1] += 1
+            key = "vm " + " ".join(f"{a}{'x' + str(b) if b > 1 else ''}" for a, b in sig)
         c = comp.setdefault(key, [0, 0.0])
         c[0] += 1
         c[1] += dur[i]
