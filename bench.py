@@ -47,6 +47,10 @@ WORKLOADS = {
                  leaf=64, eta=2.0, eps=1e-7, cfg="configs[2]"),
     "n16k": dict(n=16384, kind="uniform", thetas=[(1.0, 0.2, 1.5)], leaf=32, eta=2.0, eps=1e-8, cfg="configs[1]"),
     "n2k": dict(n=2000, kind="uniform", thetas=[(1.0, 0.0864, 0.5)], leaf=32, eta=2.0, eps=1e-8, cfg="configs[0]"),
+    # configs[3]: Monte-Carlo MLE, replicates of n = 16,384 uniform points, theta* = (1, 0.0334, 0.5),
+    # 60 Nelder-Mead evaluations each; a "step" = one replicate per rank (bench.py --workload mc)
+    "mc": dict(n=16384, kind="uniform", thetas=[(1.0, 0.0334, 0.5)], leaf=32, eta=2.0, eps=1e-6, cfg="configs[3]",
+               evals=60, start=(0.8, 0.05, 0.7)),
 }
 
 
@@ -212,6 +216,52 @@ def cpu_baseline(w, budget_s=20.0):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def run_mc(args, w):
+    """configs[3]: each rank fits its own replicates (60 Nelder-Mead evaluations each,
+    paper_1709_04419_b200.mle); value = likelihood evaluations per second, whole job."""
+    import torch
+    ws, rk, lr = dist_env()
+    torch.cuda.set_device(lr)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    from paper_1709_04419_b200.mle import mc_mle
+    reps = ws * (args.warmup + args.steps)
+    # warm-up replicates (untimed), then args.steps replicates per rank, timed
+    mc_mle(w["n"], ws * args.warmup, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"], leaf=w["leaf"],
+           rank=rk, world=ws, device=lr, seed=10_000, gather=False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(lr) as clk:
+        e0.record(stream)
+        res = mc_mle(w["n"], ws * args.steps, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
+                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{lr}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rk == 0:
+        n_evals = ws * args.steps * w["evals"]
+        line = {"metric": f"H-log-likelihood evals/sec (MC-MLE, n={w['n']})", "value": n_evals / (ms / 1e3),
+                "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{w['cfg']}: {w['evals']} Nelder-Mead evals per replicate, one replicate per "
+                                       f"rank per step (incl. its H-build and sampler), n={w['n']}, eps={w['eps']}",
+                           "parallelism": f"replicas x{ws}"},
+                "estimates_rank0": res.tolist(), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_gpu(args, w):
     import torch
     ws, rk, lr = dist_env()
@@ -348,6 +398,8 @@ def main():
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, w)
+    elif args.workload == "mc":
+        run_mc(args, w)
     else:
         run_gpu(args, w)
 

@@ -138,11 +138,6 @@ int hm_loglik_batch(hm_handle h, const hm_theta* thetas_host, int32_t n_theta,
 int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k,
               double* Z, int32_t z_on_device);
 
-/* y = C~ x (H-matrix times k vectors; Table 1 row "C~ z").  Valid after
- * hm_build/hm_assemble and before hm_cholesky (which overwrites C~).        */
-int hm_matvec(hm_handle h, const double* x, int32_t x_on_device, int32_t k,
-              double* y, int32_t y_on_device);
-
 /* Statistics.  st[0..11]: n, #dense blocks, #low-rank blocks, max rank C~,
  * max rank L~, bytes C~, bytes L~, compression ratio C~ (1 - bytes/8n^2),
  * #plan tasks, #plan waves, #kernel launches per Cholesky, widest Cholesky

@@ -56,7 +56,6 @@ def _load():
         "hm_loglik": ([P, P, I32, I32, P], C.c_int),
         "hm_loglik_batch": ([P, P, I32, P, I32, I32, P], C.c_int),
         "hm_sample": ([P, P, I32, I32, P, I32], C.c_int),
-        "hm_matvec": ([P, P, I32, I32, P, I32], C.c_int),
         "hm_stats": ([P, P], C.c_int),
         "hm_timings": ([P, P], C.c_int),
         "hm_profile": ([P, I32], C.c_int),
@@ -77,7 +76,7 @@ def _load():
 lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
-            "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_matvec", "hm_stats", "hm_timings", "hm_profile",
+            "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_stats", "hm_timings", "hm_profile",
             "hm_kernel_stats", "hm_set_exec_mode", "hm_trace", "hm_checksum",
             "hm_dense_loglik", "hm_matern_block")
 

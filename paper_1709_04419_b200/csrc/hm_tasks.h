@@ -98,6 +98,9 @@ constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
 constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
 constexpr int TR_TCH = 128;       // stacked columns staged per shared-memory chunk
 constexpr int TR_PMAX = 1023;     // pieces per truncation
+#ifndef HM_COOP_ROWFAC
+#define HM_COOP_ROWFAC 4
+#endif
 #ifndef HM_COOP_WORK_LOG2
 #define HM_COOP_WORK_LOG2 17
 #endif
@@ -148,7 +151,7 @@ inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
     // share only adds waiting), at most TR_COOP_MAX
     const int64_t g = ((int64_t)(m + q) * kmax_tot) / TR_COOP_WORK;
     const int64_t rows = (m > q ? m : q);
-    const int64_t gmax = 2 * ((rows + TR_RCH - 1) / TR_RCH);
+    const int64_t gmax = HM_COOP_ROWFAC * ((rows + TR_RCH - 1) / TR_RCH);
     int64_t n = g < 1 ? 1 : g;
     if (n > gmax) n = gmax;
     if (n > TR_COOP_MAX) n = TR_COOP_MAX;

@@ -438,10 +438,6 @@ int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k, do
     }
 }
 
-int hm_matvec(hm_handle h, const double*, int32_t, int32_t, double*, int32_t) {
-    (void)h;
-    return set_error(HM_ERR_STATE, "hm_matvec: not implemented in this build");
-}
 
 int hm_stats(hm_handle h, double st[12]) {
     try {

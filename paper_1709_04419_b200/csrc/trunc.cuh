@@ -52,7 +52,10 @@ constexpr int ORDER_MAX = 512;
 // certificate would have to capture the flat tail of truncation noise the
 // accumulated Cholesky updates carry just below eps * sigma_1: ~4x the final
 // rank measured at n = 64k.)
-constexpr double TR_STOP = 4.0;
+#ifndef HM_TR_STOP
+#define HM_TR_STOP 4.0
+#endif
+constexpr double TR_STOP = HM_TR_STOP;
 // eps from which the final SVD of the projected block uses the Gram matrix (see F3)
 constexpr double TR_GRAM_EPS = 1e-7;
 

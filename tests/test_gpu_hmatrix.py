@@ -157,3 +157,21 @@ def test_no_uninitialised_workspace_reads(hm, monkeypatch):
         H.close()
     assert np.all(np.isfinite(outs[1]))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_mc_mle_small(hm):
+    """configs[3] driver at small size: each replicate's Nelder-Mead spends its
+    budget of evaluations through the C-ABI and improves on the start."""
+    from paper_1709_04419_b200.mle import mc_mle, mle_replicate
+    truth, start = (1.0, 0.0864, 0.5), (0.7, 0.15, 0.8)
+    res = mc_mle(2000, 2, truth, start, eps=1e-6, evals=30)
+    assert res.shape == (2, 5)
+    assert np.all(np.isfinite(res)) and np.all(res[:, 4] == 30)
+    pts = uniform_iid(2000, 0)
+    Hs = hm.HMatrix(pts, truth, eps=1e-8, leaf=32)
+    Hs.cholesky()
+    Z = Hs.sample(standard_normal(2000, 1, 1))[:, 0]
+    H = hm.HMatrix(pts, start, eps=1e-6, leaf=32)
+    H.cholesky()
+    ll0 = H.loglik(Z)[0, 0]
+    assert res[0, 3] >= ll0
