@@ -56,15 +56,19 @@ extern "C" {
 /* theta = (sigma^2, ell, nu), all > 0 (Eq. 2; sec. 2.2 l.187).                  */
 typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
 
-/* H-matrix parameters.  eps: relative accuracy per admissible block (Remark 2,
- * l.166, adaptive-rank strategy; reading R4); leaf: n_min (l.211);
- * eta: admissibility parameter (reading R2); kmax: rank capacity of one
- * low-rank block, at most 240 (HM_ERR_RANK_CAP when exceeded; 0 = default 160). */
+/* H-matrix parameters.  eps: accuracy per low-rank block in the spectral norm
+ * (Remark 2, l.166, adaptive-rank strategy; reading R4): by default
+ * ABSOLUTE, eps * sigma^2 (the paper's wording; sigma^2 makes it invariant to
+ * the scale of C), or relative to the block's norm when rel_eps = 1;
+ * leaf: n_min (l.211); eta: admissibility parameter (reading R2); kmax: rank
+ * capacity of one low-rank block, at most 240 (HM_ERR_RANK_CAP when exceeded;
+ * 0 = default 160).                                                          */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
     double  eta;
     int32_t kmax;
+    int32_t rel_eps;
 } hm_params;
 
 typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */

@@ -30,7 +30,8 @@ class Theta(C.Structure):
 
 
 class Params(C.Structure):
-    _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32)]
+    _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32),
+                ("rel_eps", C.c_int32)]
 
 
 def _load():
@@ -201,13 +202,13 @@ class HMatrix:
     """
 
     def __init__(self, locs, theta, eps: float = 1e-8, leaf: int = 32, eta: float = 2.0, kmax: int = 160,
-                 device: int = 0, stream=None):
+                 device: int = 0, stream=None, rel_eps: bool = False):
         if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
             locs = _as_f64(locs)
         lp, ld = ptr_of(locs)
         self.n = int(locs.shape[0])
         self._h = C.c_void_p()
-        self.params = Params(float(eps), int(leaf), float(eta), int(kmax))
+        self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0)
         rc = lib.hm_build(lp, ld, self.n, Theta(*theta), self.params, int(device),
                           C.c_void_p(stream) if stream else None, C.byref(self._h))
         check(rc)

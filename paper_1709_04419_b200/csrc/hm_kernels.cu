@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(ACA_THREADS) k_aca(const AcaTask* __restrict__
         normS2 += 2.0 * cross + nu2 * nv2;
         ++k;
         tries = 0;
-        if (sqrt(nu2 * nv2) <= eps * sqrt(fabs(normS2))) break;
+        // eps > 0: relative to ||S_k||_F;  eps < 0: absolute |eps| (hm_params.abs_eps)
+        if (sqrt(nu2 * nv2) <= (eps > 0.0 ? eps * sqrt(fabs(normS2)) : -eps)) break;
         // ---- next pivot row: argmax |u_k| over unused rows
         double bu = 0.0;
         int bi = 0x7fffffff;

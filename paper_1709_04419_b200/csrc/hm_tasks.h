@@ -27,6 +27,8 @@ enum VmOp : uint8_t {
                      // streamed from the pool (pipelined DMMA; replaces LD, LD, GEMM triples)
     VM_TRTRI = 10,   // tile[t0] <- tile[t1]^{-1} (lower triangular, trows[t1] x trows[t1])
     VM_ADD = 11,     // tile[t0] += tile[t1]
+    VM_MGEMM_ST = 12,// pool[goff] (rows x cols, ld) = beta * pool[goff] + sum of t1 terms from terms[pad2..]
+                     // (fused "ZERO/LD t; VM_MGEMM t; ST t": accumulators go straight to HBM)
 };
 constexpr int VM_PARTIAL_TERMS = 8;   // dense-update terms per independent partial-sum task
 constexpr int NTILE = 3;   // target + two operands (TRSM/TRMM reuse tile 1 for L)

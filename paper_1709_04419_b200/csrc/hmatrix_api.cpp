@@ -52,7 +52,9 @@ struct hm_handle_s {
     int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
     DevBuf trace;        // per-task timestamps of the last executor launch (hm_trace)
     bool tracing = false;
-    bool poison = false;   // HM_POISON_RING: NaN-fill the workspace ring before every phase (tests)
+    bool poison = false;
+    bool abs_eps = true;   // block accuracy eps absolute (x sigma^2, default) or relative (rel_eps)
+    double eps_k = 0.0;    // eps as the kernels see it: > 0 relative, < 0 absolute   // HM_POISON_RING: NaN-fill the workspace ring before every phase (tests)
     int64_t trace_n = 0;
     // profiling: per kernel family (KF_*) launch counts (always) and, when
     // enabled, a CUDA event pair around every launch on the handle's stream
@@ -131,7 +133,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         if (h->tracing)
             HM_CUDA_TRY(cudaMemsetAsync((char*)h->trace.p + 32 * p.xt.size(), 0, 8 * 64 * p.xt.size(), h->stream));
         launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
-                    d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->prm.eps, h->done.as<int>(),
+                    d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->eps_k, h->done.as<int>(),
                     h->counter.as<int>(), h->epoch,
                     h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(), p.n_bars, h->stream);
         if (h->tracing) h->trace_n = (int64_t)p.xt.size();
@@ -143,7 +145,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         const int t0 = p.t_wave_begin[w], t1 = p.t_wave_begin[w + 1];
         if (t1 > t0) {
             Launch L(h, KF_TRUNC);
-            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->prm.eps, ctr,
+            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->eps_k, ctr,
                          h->stream);
         }
         if (v1 > v0) {
@@ -180,6 +182,7 @@ int max_rank(hm_handle_s* h) {
 void do_assemble(hm_handle_s* h, hm_theta th) {
     check_theta(th);
     h->theta = th;
+    h->eps_k = h->abs_eps ? -h->prm.eps * th.sigma2 : h->prm.eps;
     matern_setup(th.sigma2, th.ell, th.nu, h->mp);
     HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
     HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
@@ -192,7 +195,7 @@ void do_assemble(hm_handle_s* h, hm_theta th) {
     {
         Launch L(h, KF_ACA);
         launch_aca(h->aca.as<AcaTask>(), (int)h->P.aca.size(), h->pts.as<double>(), h->pool.as<double>(),
-                   h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->prm.eps, h->ctr.as<double>(), h->stream);
+                   h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->eps_k, h->ctr.as<double>(), h->stream);
     }
     run_phase(h, h->rec);
     HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
@@ -279,6 +282,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         h->device = device;
         h->prm = params;
         if (const char* pz = std::getenv("HM_POISON_RING")) h->poison = pz[0] == '1';
+        h->abs_eps = params.rel_eps == 0;
         if (stream) {
             h->stream = (cudaStream_t)stream;
         } else {

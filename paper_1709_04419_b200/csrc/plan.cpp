@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstring>
 #include <cstdio>
 #include <stdexcept>
 #include <utility>
@@ -184,6 +185,58 @@ struct Builder {
         }
     }
 
+    // Second peephole: "ZERO t; VM_MGEMM t; ST t -> D" and "LD t <- D; VM_MGEMM t; ST t -> D"
+    // become one VM_MGEMM_ST writing the accumulators to D directly, provided no later
+    // instruction reads t before redefining it.
+    static bool reads_tile(const VIns& I, uint8_t t) {
+        switch (I.op) {
+            case VM_ST: case VM_POTRF: case VM_TRSM_RLT: case VM_TRSM_LN: case VM_TRMM_LN: case VM_MGEMM:
+                return I.t0 == t || ((I.op == VM_TRSM_RLT || I.op == VM_TRSM_LN || I.op == VM_TRMM_LN) && I.t1 == t);
+            case VM_GEMM: return I.t1 == t || I.t2 == t || (I.t0 == t && I.beta != 0.0);
+            case VM_ADD: return I.t0 == t || I.t1 == t;
+            case VM_TRTRI: return I.t1 == t;
+            default: return false;
+        }
+    }
+    static bool defines_tile(const VIns& I, uint8_t t) {
+        return I.t0 == t && (I.op == VM_LD || I.op == VM_ZERO || (I.op == VM_GEMM && I.beta == 0.0));
+    }
+    static void fuse_mgemm_st(const std::vector<VIns>& in, std::vector<VIns>& out) {
+        size_t i = 0;
+        while (i < in.size()) {
+            bool fused = false;
+            if (i + 2 < in.size() && in[i + 1].op == VM_MGEMM && in[i + 2].op == VM_ST) {
+                const VIns &a = in[i], &m = in[i + 1], &st = in[i + 2];
+                const uint8_t t = m.t0;
+                const bool zero_head = a.op == VM_ZERO && a.t0 == t;
+                const bool ld_head = a.op == VM_LD && a.t0 == t && a.goff == st.goff && a.ld == st.ld &&
+                                     std::memcmp(&a.rows, &st.rows, sizeof(Dim)) == 0 &&
+                                     std::memcmp(&a.cols, &st.cols, sizeof(Dim)) == 0;
+                if ((zero_head || ld_head) && st.t0 == t) {
+                    bool dead = true;
+                    for (size_t j = i + 3; j < in.size(); ++j) {
+                        if (reads_tile(in[j], t)) { dead = false; break; }
+                        if (defines_tile(in[j], t)) break;
+                    }
+                    if (dead) {
+                        VIns f = st;
+                        f.op = VM_MGEMM_ST;
+                        f.t1 = (uint8_t)m.ld;            // term count (<= VM_MAX_TERMS)
+                        f.pad2 = (int32_t)m.goff;        // first term
+                        f.beta = ld_head ? 1.0 : 0.0;
+                        out.push_back(f);
+                        i += 3;
+                        fused = true;
+                    }
+                }
+            }
+            if (!fused) {
+                out.push_back(in[i]);
+                ++i;
+            }
+        }
+    }
+
     void emit_vm(Prog& pg) {
         if (pg.ins.empty()) return;
         std::sort(pg.reads.begin(), pg.reads.end());
@@ -194,7 +247,11 @@ struct Builder {
         int32_t w = wave_of(pg.reads, pg.writes, deps);
         VTask t;
         t.ins_begin = (int32_t)ph->ins.size();
-        fuse_mgemm(pg.ins, ph->ins, ph->terms);
+        {
+            std::vector<VIns> tmp;
+            fuse_mgemm(pg.ins, tmp, ph->terms);
+            fuse_mgemm_st(tmp, ph->ins);
+        }
         t.ins_count = (int32_t)ph->ins.size() - t.ins_begin;
         xraw.push_back({w, 0, (int32_t)vraw.size(), std::move(deps)});
         vraw.push_back({w, t});

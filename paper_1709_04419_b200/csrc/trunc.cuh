@@ -40,6 +40,10 @@
 namespace hm {
 
 constexpr int TR_THREADS = 256;
+
+// truncation threshold: eps > 0 relative (sigma_i > eps sigma_1), eps < 0 absolute
+// (sigma_i > |eps|; hm_params.abs_eps, the paper's Remark 2 wording)
+__device__ __forceinline__ double tr_cut(double eps, double smax) { return eps > 0.0 ? eps * smax : -eps; }
 constexpr int ORDER_MAX = 512;
 // Range-finder stopping rule.  For a Gaussian probe w, E ||R w||^2 = ||R||_F^2, so
 // the probe norms ||M w_j|| estimate ||M||_F and the projected-probe norms
@@ -258,7 +262,7 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
     __syncthreads();
     {
         int cnt = 0;
-        for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (sig[j] > eps * s_smax && sig[j] > 0.0) ? 1 : 0;
+        for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (sig[j] > tr_cut(eps, s_smax) && sig[j] > 0.0) ? 1 : 0;
         const double tot = block_sum((double)cnt, scratch);
         if (threadIdx.x == 0) {
             int r = (int)(tot + 0.5);
@@ -446,7 +450,7 @@ static __device__ int gram_pchol(const double* Gg, int ell, double eps, int cap,
     if (threadIdx.x == 0) {
         double d0 = 0.0;
         for (int i = 0; i < ell; ++i) d0 = fmax(d0, A[i * ell + i]);
-        s_cut = eps * eps * d0;
+        s_cut = (eps > 0.0) ? eps * eps * d0 : eps * eps;
     }
     __syncthreads();
     int r = 0;
@@ -651,7 +655,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         }
         __syncthreads();
         for (int j = 0; j < TR_PW; ++j) sest = fmax(sest, s_scale[j]);
-        const double thr = eps * sest * TR_STOP;
+        const double thr = (eps > 0.0 ? eps * sest : -eps) * TR_STOP;
         __syncthreads();
         for (int blk = 0; blk < TR_NB && !finished; ++blk) {
             double* Yb = W.Y + (int64_t)blk * TR_RB * m;
@@ -801,7 +805,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     flops += 4.0 * (double)ell * K * (m + q);
     bytes += 8.0 * Srows;
     const int Kw = min(q, ell);
-    const bool gram = eps >= TR_GRAM_EPS;
+    const bool gram = fabs(eps) >= TR_GRAM_EPS;
     if (gram) {
         // ---- F3 (Gram path, eps >= TR_GRAM_EPS): G = W^T W (partials spread over the group),
         // then a column-pivoted Cholesky of G stopped at eps^2 * max diag (gram_pchol): a
@@ -864,7 +868,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         {
             const double smax = W.sig[order[0]];
             int cnt = 0;
-            for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (W.sig[j] > eps * smax && W.sig[j] > 0.0) ? 1 : 0;
+            for (int j = threadIdx.x; j < kk; j += blockDim.x) cnt += (W.sig[j] > tr_cut(eps, smax) && W.sig[j] > 0.0) ? 1 : 0;
             const double tot = block_sum((double)cnt, scratch);
             if (threadIdx.x == 0) {
                 int r = (int)(tot + 0.5);

@@ -25,8 +25,12 @@ struct TermRt {
     double alpha;
 };
 
+// dst == nullptr: T0 += result (smem tile); else dst[r + c ldd] = beta dst + result for
+// r < drows, c < dcols (VM_MGEMM_ST: accumulators straight to global memory)
 __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ terms, int nt, const double* pool,
-                                         const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by) {
+                                         const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by,
+                                         double* dst = nullptr, int64_t ldd = 0, int drows = 0, int dcols = 0,
+                                         double beta = 0.0) {
     constexpr int LA = 65, LB = 65, SA = GM_BK * LA, SB = GM_BK * LB;
     __shared__ TermRt tr[VM_MAX_TERMS];
     __shared__ int s_nch;
@@ -127,6 +131,27 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
     }
     cp_async_wait<0>();
     __syncthreads();
+    if (dst) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int r = wm + a * 8 + g, c = wn + b * 8 + 2 * t4;
+                if (r < drows) {
+                    if (c < dcols) {
+                        double* p = dst + r + (int64_t)c * ldd;
+                        *p = (beta != 0.0 ? beta * __ldcg(p) : 0.0) + acc[a][b][0];
+                    }
+                    if (c + 1 < dcols) {
+                        double* p = dst + r + (int64_t)(c + 1) * ldd;
+                        *p = (beta != 0.0 ? beta * __ldcg(p) : 0.0) + acc[a][b][1];
+                    }
+                }
+            }
+        if (threadIdx.x == 0) c_by += 8.0 * drows * dcols * (beta != 0.0 ? 2.0 : 1.0);
+        __syncthreads();
+        return;
+    }
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -163,6 +188,12 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
             case VM_MGEMM: {
                 const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;   // staging: the other tiles
                 vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by);
+            } break;
+            case VM_MGEMM_ST: {
+                const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;
+                const int r = dim_eval(I.rows, ranks), c = dim_eval(I.cols, ranks);
+                vm_mgemm(T0, terms + I.pad2, I.t1, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by, pool + I.goff,
+                         I.ld, r, c, I.beta);
             } break;
             case VM_ADD: {
                 if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * tcols[I.t0];

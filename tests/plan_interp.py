@@ -34,7 +34,8 @@ DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q
 ACA = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4"),
                 ("cap", "<i4"), ("rslot", "<i4")])
 
-VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM, VM_TRTRI, VM_ADD = range(1, 12)
+VM_LD, VM_ST, VM_GEMM, VM_POTRF, VM_TRSM_RLT, VM_TRSM_LN, VM_TRMM_LN, VM_ZERO, VM_MGEMM, VM_TRTRI, VM_ADD, \
+    VM_MGEMM_ST = range(1, 13)
 TD = 64
 
 
@@ -93,8 +94,9 @@ class Interp:
     respects only the explicit dependency lists xt/xdeps (what the persistent
     executor k_exec enforces) -- a missing edge shows up as a wrong answer."""
 
-    def __init__(self, plan: Plan, eps: float, seed: int = 0, mode: str = "waves"):
+    def __init__(self, plan: Plan, eps: float, seed: int = 0, mode: str = "waves", rel_eps: bool = False):
         self.mode = mode
+        self.rel_eps = rel_eps
         self.P = plan
         self.eps = eps
         self.pool = np.zeros(plan.pool_total)
@@ -123,8 +125,14 @@ class Interp:
         self.pool[idx] = M
 
     # ---------------------------------------------------------------- assembly (oracle entries)
+    def cut(self, smax):
+        """Truncation threshold: absolute eps * sigma^2 (device default, Remark 2) or
+        relative eps * sigma_1 (rel_eps)."""
+        return self.eps * smax if self.rel_eps else self.eps * self.sigma2
+
     def assemble(self, pts_tree, theta):
         s2, ell, nu = theta
+        self.sigma2 = float(s2)
 
         def block(r0, c0, m, q):
             a = pts_tree[r0:r0 + m]
@@ -137,7 +145,7 @@ class Interp:
         for t in self.P.aca:
             M = block(int(t["r0"]), int(t["c0"]), int(t["m"]), int(t["q"]))
             U, S, Vt = np.linalg.svd(M, full_matrices=False)
-            r = int(np.sum(S > 0.25 * self.eps * S[0]))
+            r = int(np.sum(S > 0.25 * self.cut(S[0]))) if S.size else 0
             r = min(r, int(t["cap"]))
             self.gstore(int(t["u_off"]), int(t["m"]), U[:, :r] * S[:r])
             self.gstore(int(t["v_off"]), int(t["q"]), Vt[:r].T)
@@ -170,6 +178,19 @@ class Interp:
                     C = tiles[I["t0"]].copy()
                     C[:prod.shape[0], :prod.shape[1]] = I["beta"] * C[:prod.shape[0], :prod.shape[1]] + prod
                     tiles[I["t0"]] = C
+            elif op == VM_MGEMM_ST:       # pool[dst] = beta pool[dst] + sum alpha op(A) op(B)
+                r, c = self.dim(I["rows"]), self.dim(I["cols"])
+                C = self.gload(int(I["goff"]), int(I["ld"]), r, c) * float(I["beta"])
+                for tm in ph.terms[int(I["p2"]): int(I["p2"]) + int(I["t1"])]:
+                    A = self.gload(int(tm["a_off"]), int(tm["a_ld"]), self.dim(tm["a_rows"]), self.dim(tm["a_cols"]))
+                    B = self.gload(int(tm["b_off"]), int(tm["b_ld"]), self.dim(tm["b_rows"]), self.dim(tm["b_cols"]))
+                    A = A.T if tm["ta"] else A
+                    B = B.T if tm["tb"] else B
+                    k = min(A.shape[1], B.shape[0])
+                    prod = tm["alpha"] * (A[:, :k] @ B[:k, :])
+                    rr, cc = min(r, prod.shape[0]), min(c, prod.shape[1])
+                    C[:rr, :cc] += prod[:rr, :cc]
+                self.gstore(int(I["goff"]), int(I["ld"]), C)
             elif op == VM_ADD:            # t0 += t1 (same logical dims)
                 A = tiles[I["t0"]].copy()
                 B = tiles[I["t1"]]
@@ -231,7 +252,7 @@ class Interp:
         Qa, Ra = np.linalg.qr(A)
         Qb, Rb = np.linalg.qr(B)
         W, S, Zt = np.linalg.svd(Ra @ Rb.T)
-        r = int(np.sum((S > self.eps * S[0]) & (S > 0))) if S.size else 0
+        r = int(np.sum((S > self.cut(S[0])) & (S > 0))) if S.size else 0
         r = min(r, int(t["cap"]))
         self.gstore(int(t["u_out"]), m, (Qa @ W[:, :r]) * S[:r])
         self.gstore(int(t["v_out"]), q, Qb @ Zt[:r].T)
@@ -335,7 +356,7 @@ class InterpRand(Interp):
             Om = self.rng.standard_normal((q, self.RB))
             Y = A @ (B.T @ Om)
             sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0))))   # ~ ||M||_F
-            thr = self.eps * sest * 4.0          # TR_STOP: relative Frobenius certificate
+            thr = (self.eps * sest if self.rel_eps else self.eps * self.sigma2) * 4.0   # TR_STOP
             for _ in range(2):                       # BCGS2, first projection (twice)
                 Y = Y - Q @ (Q.T @ Y)
             G = Y.T @ Y                              # pivoted Cholesky-QR of the block
@@ -379,7 +400,7 @@ class InterpRand(Interp):
         if self.eps >= 1e-7:                         # TR_GRAM_EPS: pivoted Cholesky of W^T W
             G = Wm.T @ Wm
             ell = G.shape[0]
-            cut = self.eps ** 2 * float(np.max(np.diag(G)))
+            cut = (self.eps ** 2 * float(np.max(np.diag(G)))) if self.rel_eps else (self.eps * self.sigma2) ** 2
             piv = list(range(ell))
             R = np.zeros((ell, ell))
             r = 0
@@ -415,7 +436,7 @@ class InterpRand(Interp):
             return
         _, R = np.linalg.qr(Wm)
         Xp, S, Zt = np.linalg.svd(R.T)               # R^T = X' Z^T with X' = Xp S
-        r = int(np.sum((S > self.eps * S[0]) & (S > 0)))
+        r = int(np.sum((S > self.cut(S[0])) & (S > 0)))
         r = min(r, cap)
         Xr = Xp[:, :r] * S[:r]
         self.gstore(int(t["u_out"]), m, Q @ Xr)                  # U = Q X'
