@@ -159,8 +159,13 @@ int hm_timings(hm_handle h, double ms[3]);
 int hm_profile(hm_handle h, int32_t enable);
 
 /* Execution mode of the planned phases (Cholesky, solve, sampler, recompression):
- * 1 (default) = one persistent dependency-driven kernel per phase (k_exec),
- * 0 = one launch per wave and task type (k_trunc, k_vm).  Same arithmetic.     */
+ * 2 (default) = one persistent kernel per phase claiming READY tasks from
+ *     priority queues (k_exec_rq; priority = estimated longest path to the end),
+ * 1 = one persistent kernel per phase claiming tasks in topological order and
+ *     waiting for their predecessors (k_exec),
+ * 0 = one launch per wave and task type (k_trunc, k_vm).
+ * Same task DAG and arithmetic; a cooperative truncation sums its partials in
+ * a fixed order, so all modes agree to rounding.  HM_ERR_ARG for another mode. */
 int hm_set_exec_mode(hm_handle h, int32_t mode);
 
 /* Diagnostics: hm_trace(h, 1, NULL) makes the persistent executor record, for

@@ -21,6 +21,7 @@
 #include "common.h"
 #include "hm_kernels.h"
 #include "plan.h"
+#include "sched.h"
 #include "tree.h"
 
 namespace hm {
@@ -29,6 +30,7 @@ enum KFamily { KF_DGEN = 0, KF_ACA = 1, KF_TRUNC = 2, KF_VM = 3, KF_AUX = 4, KF_
 
 struct DPhase {
     DevBuf ins, vt, tt, tp, xt, xd, terms;
+    DevBuf xr, su2, qbase, slot_init, ctl_init;   // xr: xt with (dep_begin, dep_count) := successor range   // ready-queue schedule (sched.h)
     const Phase* ph = nullptr;
 };
 
@@ -48,8 +50,10 @@ struct hm_handle_s {
     DevBuf pool, pts, perm, ranks, flags, out, zio, dgen, aca, ctr;
     // persistent executor state: completion flags (== epoch when done) and claim counter
     DevBuf done, counter, bars;
+    DevBuf rq_cnt, rq_slot, rq_ctl;   // ready-queue executor: arrival counters, queue slots, {head, tail} + finished
     int epoch = 0;
-    int exec_mode = 1;   // 1 = persistent dependency-driven executor, 0 = one launch per wave
+    int exec_mode = 2;   // 2 = persistent ready-queue executor, 1 = persistent topological-claim executor,
+                         // 0 = one launch per wave
     DevBuf trace;        // per-task timestamps of the last executor launch (hm_trace)
     bool tracing = false;
     bool poison = false;
@@ -93,6 +97,22 @@ void upload_phase(DPhase& d, const Phase& p, cudaStream_t st) {
     upload(d.xt, p.xt, st);
     upload(d.terms, p.terms, st);
     upload(d.xd, p.xdeps, st);
+    Sched sc;
+    build_sched(p, sc);
+    {
+        std::vector<XTask> xr(p.xt);
+        for (size_t i = 0; i < xr.size(); ++i) {
+            xr[i].dep_begin = sc.succ_begin[i];
+            xr[i].dep_count = sc.succ_begin[i + 1] - sc.succ_begin[i];
+        }
+        upload(d.xr, xr, st);
+        HM_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    upload(d.su2, sc.succ2, st);
+    upload(d.qbase, sc.qbase, st);
+    upload(d.slot_init, sc.slot_init, st);
+    upload(d.ctl_init, sc.ctl_init, st);
+    HM_CUDA_TRY(cudaStreamSynchronize(st));   // sc's host vectors die here
     d.ph = &p;
 }
 
@@ -127,6 +147,19 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
     int* ranks = h->ranks.as<int>();
     int* flags = h->flags.as<int>();
     double* ctr = h->ctr.as<double>();
+    if (h->exec_mode == 2) {
+        Launch L(h, KF_EXEC);
+        if (h->tracing)
+            HM_CUDA_TRY(cudaMemsetAsync((char*)h->trace.p + 32 * p.xt.size(), 0, 8 * 64 * p.xt.size(), h->stream));
+        launch_exec_rq(d.xr.as<XTask>(), (int)p.xt.size(), d.su2.as<int32_t>(), d.qbase.as<int32_t>(), d.slot_init.as<int32_t>(), d.ctl_init.as<int32_t>(),
+                       h->rq_cnt.as<int>(), h->rq_slot.as<int>(), h->rq_ctl.as<int>(), d.vt.as<VTask>(),
+                       d.ins.as<VIns>(), d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags,
+                       ctr, h->eps_k, h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(),
+                       p.n_bars, h->stream);
+        if (h->tracing) h->trace_n = (int64_t)p.xt.size();
+        HM_CUDA_TRY(cudaGetLastError());
+        return;
+    }
     if (h->exec_mode == 1) {
         Launch L(h, KF_EXEC);
         ++h->epoch;
@@ -314,6 +347,9 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
             h->done.alloc(sizeof(int) * mx);
             HM_CUDA_TRY(cudaMemsetAsync(h->done.p, 0, sizeof(int) * mx, h->stream));
             h->counter.alloc(sizeof(int) * 4);
+            h->rq_cnt.alloc(sizeof(int) * mx);
+            h->rq_slot.alloc(sizeof(int) * mx);
+            h->rq_ctl.alloc(sizeof(int) * (2 * RQ_NQ + 2));
             int nb = 1;
             for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) nb = std::max(nb, ph->n_bars);
             h->bars.alloc(sizeof(int) * nb);
@@ -566,7 +602,8 @@ int hm_trace(hm_handle h, int32_t enable, const char* path) {
 
 int hm_set_exec_mode(hm_handle h, int32_t mode) {
     if (!h) return set_error(HM_ERR_ARG, "null handle");
-    if (mode != 0 && mode != 1) return set_error(HM_ERR_ARG, "mode must be 0 (waves) or 1 (persistent)");
+    if (mode < 0 || mode > 2)
+        return set_error(HM_ERR_ARG, "mode must be 0 (waves), 1 (persistent, topological claim) or 2 (persistent, ready queues)");
     h->exec_mode = mode;
     return HM_OK;
 }

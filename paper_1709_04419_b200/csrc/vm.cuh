@@ -30,7 +30,7 @@ struct TermRt {
 __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ terms, int nt, const double* pool,
                                          const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by,
                                          double* dst = nullptr, int64_t ldd = 0, int drows = 0, int dcols = 0,
-                                         double beta = 0.0) {
+                                         double beta = 0.0, unsigned long long* stt = nullptr) {
     constexpr int LA = 65, LB = 65, SA = GM_BK * LA, SB = GM_BK * LB;
     __shared__ TermRt tr[VM_MAX_TERMS];
     __shared__ int s_nch;
@@ -62,6 +62,7 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
             c_by += 8.0 * ((double)tr[t].M + tr[t].N) * tr[t].K;
         }
         s_nch = c;
+        if (stt) stt[2] = gtimer();
     }
     __syncthreads();
     const int nch = s_nch;
@@ -101,23 +102,19 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         ++ik;
     };
     int ct = 0, ck = 0;                                  // compute cursor
-#pragma unroll
-    for (int s = 0; s < GM_NS - 1; ++s) {
-        if (s < nch) issue(s);
-        cp_async_commit();
-    }
-    for (int s = 0; s < nch; ++s) {
-        cp_async_wait<GM_NS - 2>();
-        __syncthreads();
-        if (s + GM_NS - 1 < nch) issue(s + GM_NS - 1);
-        cp_async_commit();
+    auto compute = [&](int s) {
         while (ct < nt && ck >= (tr[ct].K + GM_BK - 1) / GM_BK) { ++ct; ck = 0; }
         const double al = tr[ct].alpha;
+        // fragments outside this term's op(A) rows / op(B) columns get zeros from it: skip
+        // their DMMAs (warp-uniform; low-rank factors are often much narrower than 64)
+        const int am = tr[ct].M - wm, bn = tr[ct].N - wn, kr = tr[ct].K - ck * GM_BK;
         ++ck;
+        if (am <= 0 || bn <= 0) return;
         const double* as = As + (s % GM_NS) * SA;
         const double* bs = Bs + (s % GM_NS) * SB;
 #pragma unroll
         for (int kk = 0; kk < GM_BK; kk += 4) {
+            if (kk >= kr) break;
             double af[2], bf[4];
 #pragma unroll
             for (int a = 0; a < 2; ++a) af[a] = al * as[(kk + t4) * LA + wm + a * 8 + g];
@@ -126,11 +123,35 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) dmma_884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+                for (int b = 0; b < 4; ++b)
+                    if (a * 8 < am && b * 8 < bn) dmma_884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    };
+    if (nch <= GM_NS) {
+        // short sums (the latency-bound tasks on the Cholesky's critical path): every chunk
+        // in flight at once, a single wait
+        for (int s = 0; s < nch; ++s) issue(s);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        for (int s = 0; s < nch; ++s) compute(s);
+    } else {
+#pragma unroll
+        for (int s = 0; s < GM_NS - 1; ++s) {
+            issue(s);
+            cp_async_commit();
+        }
+        for (int s = 0; s < nch; ++s) {
+            cp_async_wait<GM_NS - 2>();
+            __syncthreads();
+            if (s + GM_NS - 1 < nch) issue(s + GM_NS - 1);
+            cp_async_commit();
+            compute(s);
         }
     }
     cp_async_wait<0>();
     __syncthreads();
+    if (stt && threadIdx.x == 0) stt[3] = gtimer();
     if (dst) {
 #pragma unroll
         for (int a = 0; a < 2; ++a)
@@ -150,6 +171,7 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
             }
         if (threadIdx.x == 0) c_by += 8.0 * drows * dcols * (beta != 0.0 ? 2.0 : 1.0);
         __syncthreads();
+        if (stt && threadIdx.x == 0) stt[4] = gtimer();
         return;
     }
 #pragma unroll
@@ -165,12 +187,15 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
 
 // Execute one tile-VM program with the CTA (TTHREADS threads); sm = NTILE tiles.
 __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict__ ins, const VTerm* __restrict__ terms,
-                                       double* pool, const int* ranks, int* flags, double* ctr, double* sm) {
+                                       double* pool, const int* ranks, int* flags, double* ctr, double* sm,
+                                       unsigned long long* stt = nullptr) {
     __shared__ int trows[NTILE], tcols[NTILE];
+    if (stt && threadIdx.x == 0) stt[0] = gtimer();
     __shared__ double s_log;
     double c_fl = 0.0, c_by = 0.0;   // algorithmic flops / bytes of this program (thread 0)
     for (int pc = 0; pc < task.ins_count; ++pc) {
         const VIns I = ins[task.ins_begin + pc];
+        if (stt && pc == 0 && threadIdx.x == 0) stt[1] = gtimer();
         double* T0 = sm + (int)I.t0 * TSZ;
         switch (I.op) {
             case VM_LD: {
@@ -193,7 +218,7 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
                 const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;
                 const int r = dim_eval(I.rows, ranks), c = dim_eval(I.cols, ranks);
                 vm_mgemm(T0, terms + I.pad2, I.t1, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by, pool + I.goff,
-                         I.ld, r, c, I.beta);
+                         I.ld, r, c, I.beta, task.ins_count == 1 ? stt : nullptr);
             } break;
             case VM_ADD: {
                 if (threadIdx.x == 0) c_fl += (double)trows[I.t0] * tcols[I.t0];

@@ -102,15 +102,16 @@ def test_errors(hm):
 
 @pytest.mark.parametrize("n,leaf", [(2000, 32), (3000, 16)])
 def test_exec_modes_identical(hm, n, leaf):
-    """Persistent dependency-driven executor (default) vs one launch per wave.
-    Same task DAG; the persistent executor may split a wide truncation over
-    several CTAs (different summation order of its partial reductions), so the
-    results agree to rounding (1e-10 relative), not bit for bit."""
+    """Persistent ready-queue executor (default, mode 2), persistent
+    topological-claim executor (mode 1) and one launch per wave (mode 0).  Same
+    task DAG; a persistent executor may split a wide truncation over several
+    CTAs (different summation order of its partial reductions), so the results
+    agree to rounding (1e-10 relative), not bit for bit."""
     pts = uniform_iid(n, seed=21)
     theta = (1.0, 0.0864, 0.5)
     Z = standard_normal(n, 2, seed=22)
     outs = []
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         H = hm.HMatrix(pts, theta, eps=1e-7, leaf=leaf, eta=2.0)
         H.set_exec_mode(mode)
         H.assemble(theta)
@@ -118,8 +119,9 @@ def test_exec_modes_identical(hm, n, leaf):
         outs.append(H.loglik(Z))
         H.close()
     np.testing.assert_allclose(outs[1], outs[0], rtol=1e-10)
+    np.testing.assert_allclose(outs[2], outs[0], rtol=1e-10)
     oll, _, _ = od.loglik(pts, Z, theta)
-    np.testing.assert_allclose(outs[1][:, 0], oll, rtol=1e-5)
+    np.testing.assert_allclose(outs[2][:, 0], oll, rtol=1e-5)
 
 
 def test_repeat_evaluations_bit_identical(hm):

@@ -82,6 +82,50 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
         c = comp.setdefault(key, [0, 0.0])
         c[0] += 1
         c[1] += dur[i]
+    # single-instruction MGEMM_ST tasks on the critical path by number of terms
+    hist = {}
+    for i in path:
+        x = ph.xt[i]
+        if x["kind"] != 0:
+            continue
+        v = ph.vt[x["idx"]]
+        insv = ph.ins[v["ins_begin"]: v["ins_begin"] + v["ins_count"]]
+        if len(insv) == 1 and int(insv["op"][0]) == 12:
+            nt = int(insv["t1"][0])
+            b = 1 if nt <= 1 else 2 if nt <= 2 else 4 if nt <= 4 else 8 if nt <= 8 else 16 if nt <= 16 else 64 if nt <= 64 else 999
+            h = hist.setdefault(b, [0, 0.0, 0])
+            h[0] += 1
+            h[1] += dur[i]
+            h[2] += nt
+    # stage stamps of single-instruction MGEMM_ST tasks on the critical path (ns since claim)
+    sel = []
+    for i in path:
+        x = ph.xt[i]
+        if x["kind"] == 0:
+            v = ph.vt[x["idx"]]
+            if v["ins_count"] == 1 and int(ph.ins["op"][v["ins_begin"]]) == 12 and stg[i, 5] > 0:
+                sel.append(i)
+    if sel:
+        sel = np.array(sel)
+        c0 = tr[sel, 0].astype(np.float64)
+        st = [(stg[sel, k].astype(np.float64) - c0).mean() * 1e-3 for k in range(6)]
+        lines.append("  CP MGEMM_ST stage stamps (us after claim): start %.2f ins %.2f terms %.2f compute %.2f store %.2f"
+                     " completion %.2f end %.2f (n=%d)" % (*st, (tr[sel, 2].astype(np.float64) - c0).mean() * 1e-3, len(sel)))
+        one = sel[[int(ph.ins["t1"][ph.vt[ph.xt[i]["idx"]]["ins_begin"]]) == 1 for i in sel]]
+        if one.size:
+            c0 = tr[one, 0].astype(np.float64)
+            st = [(stg[one, k].astype(np.float64) - c0).mean() * 1e-3 for k in range(6)]
+            lines.append("    1-term only:                                start %.2f ins %.2f terms %.2f compute %.2f store %.2f"
+                         " completion %.2f (n=%d)" % (*st, len(one)))
+        # the gap between a CP task's end and its CP successor's claim (queue latency)
+        pos = {int(j): k for k, j in enumerate(path)}
+        gaps = [claim[path[k + 1]] - end[path[k]] for k in range(len(path) - 1)]
+        lines.append("  CP hand-over gap (claim of next - end of previous), us: mean %.2f median %.2f total %.1f ms"
+                     % (np.mean(gaps), np.median(gaps), np.sum(np.maximum(gaps, 0)) / 1e3))
+    lines.append("  critical-path MGEMM_ST tasks by terms (<=b: count, ms, mean us, mean terms):")
+    for b in sorted(hist):
+        c, d, nt = hist[b]
+        lines.append(f"    <= {b:4d}: {c:6d} {d / 1e3:9.3f} {d / c:8.1f} {nt / c:7.1f}")
     lines.append("  critical-path composition (count, ms):")
     for k, (cnt, d) in sorted(comp.items(), key=lambda kv: -kv[1][1])[:14]:
         lines.append(f"    {k:40s} {cnt:6d} {d / 1e3:9.3f}")
