@@ -259,7 +259,8 @@ class HMatrix:
     KERNEL_FAMILIES = ("k_dense_gen", "k_aca", "k_trunc", "k_vm", "k_aux", "k_exec")
 
     def set_exec_mode(self, mode: int):
-        """1 = persistent dependency-driven executor (default), 0 = one launch per wave."""
+        """2 = persistent ready-queue executor (default), 1 = persistent topological-claim
+        executor, 0 = one launch per wave."""
         check(lib.hm_set_exec_mode(self._h, int(mode)))
 
     def trace(self, enable: bool, path: str | None = None):

@@ -92,7 +92,14 @@ struct TTask {
 };
 
 // k_trunc algorithm selection and workspace (trunc.cuh; planner sizes the workspace)
-constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs
+constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs ...
+constexpr int TR_EXACT_MMAX = 512;   // ... on blocks with at most this many rows and columns: the
+                                     // single-CTA Householder QR of a taller factor is HBM-latency
+                                     // bound (~25 ms at 8192 x 160); those take the cooperative
+                                     // randomized path instead
+HM_HD inline bool trunc_exact_path(int32_t m, int32_t q, int32_t kmax_tot) {
+    return kmax_tot <= TR_EXACT_K && m <= TR_EXACT_MMAX && q <= TR_EXACT_MMAX;
+}
 constexpr int TR_RB = 16;         // probes per block of the randomized range finder
 constexpr int TR_NB = 3;          // blocks per pass over the stacks
 constexpr int TR_PW = TR_RB * TR_NB;
@@ -140,14 +147,14 @@ HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t
     return w;
 }
 inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot, int32_t nsub) {
-    if (kmax_tot <= TR_EXACT_K) {
+    if (trunc_exact_path(m, q, kmax_tot)) {
         const int64_t K = kmax_tot;
         return ((int64_t)m + q + 2 * K + 8) * K + 64;
     }
     return trunc_ws_layout(nullptr, m, q, cap, kmax_tot, nsub).total;
 }
 inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
-    if (kmax_tot <= TR_EXACT_K) return 1;
+    if (trunc_exact_path(m, q, kmax_tot)) return 1;
     // one CTA per TR_COOP_WORK of stacked data, at most two per 64-row chunk of the
     // larger side (a group must assemble before it starts: more CTAs than rows to
     // share only adds waiting), at most TR_COOP_MAX

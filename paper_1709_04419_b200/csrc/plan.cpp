@@ -1003,19 +1003,29 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
         P.tmp_off = bld.alloc(nslots * Builder::TMP_SLOT);
         for (int64_t i = 0; i < nslots; ++i) bld.tmp_res.push_back(bld.new_res(1));
     }
-    // truncation workspace ring: starts at >= 4x the largest recompression workspace
-    // (min 128 MiB) and grows to >= 4x the largest workspace the Cholesky emits
+    // truncation workspace ring: starts at >= 4x the largest recompression workspace and,
+    // within 1 GiB, at the sum of all of them (the recompressions are independent: ring
+    // reuse is their only dependency, so a small ring would chain them); grows to >= 4x
+    // the largest workspace the Cholesky emits
+    std::vector<int32_t> lr_order;
     {
-        int64_t maxs = 0;
+        int64_t maxs = 0, sum = 0;
         for (int32_t b = 0; b < nb; ++b) {
             const BStore& s = P.bs[b];
             if (s.kind != ST_LR) continue;
-            maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K, 1));
+            lr_order.push_back(b);
+            const int64_t w = trunc_ws_size(s.m, s.p, s.cap, s.cap, trunc_nsub(s.m, s.p, s.cap));
+            maxs = std::max(maxs, w);
+            sum += w;
             maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, 1));
         }
         bld.ring_chunk = int64_t(1) << 16;   // 512 KiB
-        const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 24, 64 * maxs));
+        const int64_t want = std::max<int64_t>(4 * maxs, std::min<int64_t>(int64_t(1) << 27, sum + sum / 8));
         bld.grow_ring((want + bld.ring_chunk - 1) / bld.ring_chunk);
+        // largest first: the long recompressions start at once and the ring wraps onto short ones
+        std::stable_sort(lr_order.begin(), lr_order.end(), [&](int32_t a, int32_t b) {
+            return (int64_t)P.bs[a].m + P.bs[a].p > (int64_t)P.bs[b].m + P.bs[b].p;
+        });
     }
     // assembly tasks
     for (int32_t b = 0; b < nb; ++b) {
@@ -1032,8 +1042,7 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     bld.pend.assign(nb, Pend());
     // recompression of every ACA block: a truncation with the block itself as the only piece
     bld.begin_phase(P.recompress);
-    for (int32_t b = 0; b < nb; ++b)
-        if (P.bs[b].kind == ST_LR) bld.flush_lr(b, true);
+    for (int32_t b : lr_order) bld.flush_lr(b, true);
     bld.end_phase();
     // H-Cholesky
     bld.begin_phase(P.chol);

@@ -922,7 +922,7 @@ __device__ __forceinline__ void trunc_run(const TTask& t, const TPiece* __restri
                                           int* bar = nullptr, unsigned long long* stt = nullptr) {
     int K = 0;
     for (int p = 0; p < t.piece_count; ++p) K += dim_eval(pieces[t.piece_begin + p].w, ranks);
-    if (t.kmax_tot <= TR_EXACT_K) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
+    if (trunc_exact_path(t.m, t.q, t.kmax_tot)) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
     else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr, dsm, sub, nsub, bar, stt);
 }
 

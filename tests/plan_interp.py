@@ -333,10 +333,11 @@ class InterpRand(Interp):
     W = M^T Q, QR, SVD of R^T,
     U = Q X', V = W X' Sigma^-2.  Used to check that algorithm on the CPU."""
     RB = 16
-    EXACT_K = 160
+    EXACT_K = 160      # hm_tasks.h TR_EXACT_K / TR_EXACT_MMAX (trunc_exact_path)
+    EXACT_MMAX = 512
 
     def trunc(self, ph, t):
-        if int(t["kmax_tot"]) <= self.EXACT_K:
+        if int(t["kmax_tot"]) <= self.EXACT_K and int(t["m"]) <= self.EXACT_MMAX and int(t["q"]) <= self.EXACT_MMAX:
             return super().trunc(ph, t)
         m, q, cap = int(t["m"]), int(t["q"]), int(t["cap"])
         As, Bs = [], []

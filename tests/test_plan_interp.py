@@ -57,6 +57,21 @@ def test_randomized_truncation_algorithm(tmp_path, eps, tol):
     np.testing.assert_allclose(ll, oll, rtol=tol)
 
 
+def test_randomized_recompression_of_tall_blocks(tmp_path):
+    """Recompressions of ACA blocks taller than TR_EXACT_MMAX (512) take the
+    cooperative randomized path (hm_tasks.h trunc_exact_path): on a thin strip
+    (near 1-D, so 600 x 600 blocks are admissible) the replayed plan still
+    matches the dense oracle at the accuracy eps allows."""
+    rng = np.random.default_rng(3)
+    pts = np.stack([rng.random(2400), 0.01 * rng.random(2400)], axis=1)
+    ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.2, 0.5), 32, 2.0, 1e-8, kmax=160, seed=0, k=1,
+                                         cls=InterpRand)
+    P = Plan(str(tmp_path / "plan.bin"))
+    tall = [(int(x["m"]), int(x["kmax_tot"])) for x in P.recompress.tt if int(x["m"]) > 512]
+    assert tall, "no recompression above TR_EXACT_MMAX in this geometry"
+    np.testing.assert_allclose(ll, oll, rtol=1e-6)
+
+
 def test_planner_general_nu_mesh(tmp_path):
     pts = perturbed_mesh(24, 0.4, seed=4)
     ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.3, 0.2, 1.5), 16, 2.0, 1e-10)
