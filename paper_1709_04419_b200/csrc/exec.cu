@@ -108,7 +108,13 @@ __device__ __forceinline__ void st_relaxed_gpu(int* p, int v) {
 
 // xr: the phase's tasks with (dep_begin, dep_count) replaced by their successor range in
 // succ2 = {successor, rq_pack(need, nsub, queue)} pairs (sched.h)
-__global__ void __launch_bounds__(TTHREADS, 2)
+// one CTA per SM: the whole register file (no spills of the truncation code) and an
+// SM of its own for a critical-path task beat a second resident CTA (measured at
+// n = 64k: H-Cholesky 652 -> ~560 ms)
+#ifndef HM_EXEC_RQ_MINB
+#define HM_EXEC_RQ_MINB 1
+#endif
+__global__ void __launch_bounds__(TTHREADS, HM_EXEC_RQ_MINB)
     k_exec_rq(const XTask* __restrict__ xr, int nx, const int2* __restrict__ succ2, const int32_t* __restrict__ qbase,
               int* cnt, int* slot, int* ctl, const VTask* __restrict__ vt, const VIns* __restrict__ ins,
               const VTerm* __restrict__ terms, const TTask* __restrict__ tt, const TPiece* __restrict__ tp,
@@ -240,22 +246,31 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     }
 }
 
-int exec_grid() {
-    static int grid = 0;
-    if (grid) return grid;
-    HM_CUDA_TRY(cudaFuncSetAttribute(k_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM));
-    HM_CUDA_TRY(cudaFuncSetAttribute(k_exec_rq, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM));
+static int grid_of(const void* fn, int& cache) {
+    if (cache) return cache;
+    HM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM));
     int dev = 0, sms = 0, occ = 0;
     HM_CUDA_TRY(cudaGetDevice(&dev));
     HM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exec, TTHREADS, EXEC_SMEM));
+    HM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TTHREADS, EXEC_SMEM));
     if (occ < 1) occ = 1;
-    grid = sms * occ;
+    int grid = sms * occ;
     if (const char* g = std::getenv("HM_EXEC_GRID")) {   // debug: fewer persistent CTAs
         const int v = std::atoi(g);
         if (v > 0 && v < grid) grid = v;
     }
+    cache = grid;
     return grid;
+}
+
+int exec_grid() {
+    static int g = 0;
+    return grid_of((const void*)k_exec, g);
+}
+
+int exec_grid_rq() {
+    static int g = 0;
+    return grid_of((const void*)k_exec_rq, g);
 }
 
 void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const VTerm* terms,
@@ -275,7 +290,7 @@ void launch_exec_rq(const XTask* xr, int nx, const int32_t* succ2, const int32_t
                     const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps,
                     unsigned long long* trace, int* bars, int nbars, cudaStream_t st) {
     if (nx <= 0) return;
-    const int grid = exec_grid();
+    const int grid = exec_grid_rq();
     if (grid <= RQ_NCOOP * (TR_COOP_MAX - 1)) throw ApiError(HM_ERR_ARG, "ready-queue executor needs more resident CTAs");
     HM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * nx, st));
     HM_CUDA_TRY(cudaMemcpyAsync(slot, slot_init, sizeof(int) * nx, cudaMemcpyDeviceToDevice, st));

@@ -18,6 +18,7 @@ void vm_set_attr();
 void launch_vm(const VTask* t, int n, const VIns* ins, const VTerm* terms, double* pool, const int* ranks, int* flags,
                double* ctr, cudaStream_t st);
 int exec_grid();
+int exec_grid_rq();
 void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, const VIns* ins, const VTerm* terms,
                  const TTask* tt,
                  const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps, int* done,

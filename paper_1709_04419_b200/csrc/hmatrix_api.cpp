@@ -354,6 +354,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
             for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) nb = std::max(nb, ph->n_bars);
             h->bars.alloc(sizeof(int) * nb);
             exec_grid();
+            exec_grid_rq();
         }
         HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
         h->out.alloc(sizeof(double) * 3 * h->P.zw);

@@ -98,7 +98,25 @@ __device__ __forceinline__ void tile_zero(double* T) {
 // Load rows x cols (col-major, leading dim ld) from global into a zero-padded tile.
 // (ld.global.cg: the source may have been written by another CTA of the same
 // persistent kernel, so the read-only / L1 paths are not used)
+// All 16 loads of a thread are issued before the first store to shared memory, so a
+// tile costs one global-memory latency, not sixteen (TTHREADS = 256 threads).
 __device__ __forceinline__ void tile_load(double* T, const double* G, int64_t ld, int rows, int cols) {
+    if (blockDim.x == TTHREADS) {
+        constexpr int PER = TD * TD / TTHREADS;
+        double v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + u * TTHREADS;
+            const int r = idx & (TD - 1), c = idx >> 6;
+            v[u] = (r < rows && c < cols) ? __ldcg(G + (int64_t)c * ld + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + u * TTHREADS;
+            T[(idx >> 6) * TLD + (idx & (TD - 1))] = v[u];
+        }
+        return;
+    }
     for (int idx = threadIdx.x; idx < TD * TD; idx += blockDim.x) {
         const int r = idx & (TD - 1), c = idx >> 6;
         T[c * TLD + r] = (r < rows && c < cols) ? __ldcg(G + (int64_t)c * ld + r) : 0.0;
@@ -116,28 +134,33 @@ __device__ __forceinline__ void tile_store(const double* T, double* __restrict__
 // Returns (to all threads) the number of failed pivots (0 on success); on
 // failure the offending pivot is replaced by 1 so the factor stays finite.
 // *logdiag_sum receives sum_i log A_ii of the factor (thread 0).
+// Left-looking by columns (the Cholesky is on the factorisation's critical path:
+// latency matters, not flops): for column j, a group of 4 lanes per row i >= j
+// forms A_ij - sum_{k<j} L_ik L_jk (strided over k, shuffle-reduced); then the
+// pivot and the scaling.  Two CTA barriers per column.  Needs blockDim.x = 256.
 __device__ __forceinline__ int tile_potrf(double* A, int m, double* logdiag_sum) {
     __shared__ int s_fail;
-    __shared__ double s_piv;
+    __shared__ double s_v[TD];
+    const int r = threadIdx.x >> 2, p = threadIdx.x & 3;
     if (threadIdx.x == 0) s_fail = 0;
-    __syncthreads();
     for (int j = 0; j < m; ++j) {
-        if (threadIdx.x == 0) {
-            double d = A[j * TLD + j];
-            if (!(d > 0.0)) { s_fail += 1; d = 1.0; }
-            s_piv = sqrt(d);
-            A[j * TLD + j] = s_piv;
-        }
+        double sum = 0.0;
+        const bool act = r >= j && r < m;
+        if (act)
+            for (int k = p; k < j; k += 4) sum += A[k * TLD + r] * A[k * TLD + j];
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (act && p == 0) s_v[r] = A[j * TLD + r] - sum;
         __syncthreads();
-        const double piv = s_piv;
-        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) A[j * TLD + i] /= piv;
-        __syncthreads();
-        // trailing update of the lower triangle: A[i][c] -= A[i][j] A[c][j], j < c <= i
-        const int rem = m - j - 1;
-        for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
-            const int i = j + 1 + idx % rem;
-            const int c = j + 1 + idx / rem;
-            if (c <= i) A[c * TLD + i] -= A[j * TLD + i] * A[j * TLD + c];
+        if (act && p == 0) {
+            const double d = s_v[j];
+            const double piv = (d > 0.0) ? sqrt(d) : 1.0;
+            if (r == j) {
+                A[j * TLD + j] = piv;
+                if (!(d > 0.0)) s_fail += 1;
+            } else {
+                A[j * TLD + r] = s_v[r] / piv;
+            }
         }
         __syncthreads();
     }
@@ -146,10 +169,12 @@ __device__ __forceinline__ int tile_potrf(double* A, int m, double* logdiag_sum)
         const int i = idx % m, c = idx / m;
         if (c > i) A[c * TLD + i] = 0.0;
     }
-    if (logdiag_sum != nullptr && threadIdx.x == 0) {
+    if (logdiag_sum != nullptr && threadIdx.x < 32) {
         double s = 0.0;
-        for (int j = 0; j < m; ++j) s += log(A[j * TLD + j]);
-        *logdiag_sum = s;
+        for (int j = threadIdx.x; j < m; j += 32) s += log(A[j * TLD + j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) *logdiag_sum = s;
     }
     __syncthreads();
     return s_fail;
@@ -197,18 +222,26 @@ __device__ __forceinline__ void tile_add(double* A, const double* B) {
     __syncthreads();
 }
 
-// X <- L^{-1} for the m x m lower-triangular tile L (X lower, zero elsewhere): column j
-// solves L x = e_j by forward substitution (one thread per column).  X != L.
+// X <- L^{-1} for the m x m lower-triangular tile L (X lower, zero elsewhere).  Column j
+// of X solves L x = e_j by forward substitution; each column is owned by a group of 4
+// lanes of one warp (dot products strided over k, shuffle-reduced), so the row-by-row
+// dependency stays inside the group: no CTA barrier until the end.  X != L;
+// needs blockDim.x = 256.
 __device__ __forceinline__ void tile_trtri(double* X, const double* L, int m) {
     tile_zero(X);
     __syncthreads();
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        X[j * TLD + j] = 1.0 / L[j * TLD + j];
-        for (int i = j + 1; i < m; ++i) {
-            double s = 0.0;
-            for (int k = j; k < i; ++k) s += L[k * TLD + i] * X[j * TLD + k];
-            X[j * TLD + i] = -s / L[i * TLD + i];
-        }
+    const int j = threadIdx.x >> 2, p = threadIdx.x & 3;
+    const bool act = j < m;
+    if (act && p == 0) X[j * TLD + j] = 1.0 / L[j * TLD + j];
+    __syncwarp();
+    for (int i = 1; i < m; ++i) {
+        double sum = 0.0;
+        if (act && i > j)
+            for (int k = j + p; k < i; k += 4) sum += L[k * TLD + i] * X[j * TLD + k];
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (act && i > j && p == 0) X[j * TLD + i] = -sum / L[i * TLD + i];
+        __syncwarp();
     }
     __syncthreads();
 }
