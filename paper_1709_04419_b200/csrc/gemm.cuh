@@ -21,7 +21,12 @@
 namespace hm {
 
 constexpr int GM_BK = 16;
-constexpr int GM_NS = 4;
+constexpr int GM_NS = 4;      // stages of the tile-VM products (staged in two 64 x 68 tiles)
+#ifndef HM_GM_NSC
+#define HM_GM_NSC 8
+#endif
+constexpr int GM_NSC = HM_GM_NSC;   // stages of cta_gemm (truncations): with one CTA per SM
+                                    // the deeper pipeline keeps ~100 KB of loads in flight
 
 struct GOp {
     const double* p;
@@ -32,7 +37,7 @@ __device__ __forceinline__ GOp gop(const double* p, int64_t ld, bool trans) { re
 
 template <int BM, int BN>
 constexpr int gemm_smem_doubles() {
-    return GM_NS * (GM_BK * (BM + 1) + GM_BK * (BN + 1));
+    return GM_NSC * (GM_BK * (BM + 1) + GM_BK * (BN + 1));
 }
 
 __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, bool valid) {
@@ -53,7 +58,7 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
     constexpr int SA = GM_BK * LA, SB = GM_BK * LB;      // doubles per stage
     constexpr int NA = (GM_BK * BM + 255) / 256, NB = (GM_BK * BN + 255) / 256;
     double* As = smem;                                   // [stage][k][i]
-    double* Bs = smem + GM_NS * SA;                      // [stage][k][j]
+    double* Bs = smem + GM_NSC * SA;                      // [stage][k][j]
     const bool tA = A.trans, tB = B.trans;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -64,8 +69,8 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
         const int i0 = (tile % tm) * BM, j0 = (tile / tm) * BN;
         auto issue = [&](int kc) {                       // chunk kc -> stage kc % NS
             const int k0 = kc * GM_BK;
-            double* as = As + (kc % GM_NS) * SA;
-            double* bs = Bs + (kc % GM_NS) * SB;
+            double* as = As + (kc % GM_NSC) * SA;
+            double* bs = Bs + (kc % GM_NSC) * SB;
 #pragma unroll
             for (int e = 0; e < NA; ++e) {
                 const int idx = threadIdx.x + e * 256;
@@ -98,17 +103,17 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
             for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         __syncthreads();                                 // previous tile's readers are done with the stages
 #pragma unroll
-        for (int s = 0; s < GM_NS - 1; ++s) {
+        for (int s = 0; s < GM_NSC - 1; ++s) {
             if (s < nk) issue(s);
             cp_async_commit();
         }
         for (int kc = 0; kc < nk; ++kc) {
-            cp_async_wait<GM_NS - 2>();
+            cp_async_wait<GM_NSC - 2>();
             __syncthreads();
-            if (kc + GM_NS - 1 < nk) issue(kc + GM_NS - 1);
+            if (kc + GM_NSC - 1 < nk) issue(kc + GM_NSC - 1);
             cp_async_commit();
-            const double* as = As + (kc % GM_NS) * SA;
-            const double* bs = Bs + (kc % GM_NS) * SB;
+            const double* as = As + (kc % GM_NSC) * SA;
+            const double* bs = Bs + (kc % GM_NSC) * SB;
 #pragma unroll
             for (int kk = 0; kk < GM_BK; kk += 4) {
                 double af[FM], bf[FN];

@@ -118,9 +118,23 @@ constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
 
 struct TruncWs {                  // randomized-path workspace (doubles unless noted)
     double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp,
-        *Gp2, *Ypart, *Wpart;
+        *Gp2, *Ypart, *Wpart, *Rpart;
     int64_t total;
 };
+// Reduction split of the two products with a long inner dimension, T^T = Omega^T V_stack
+// (over q) and P^T = Q^T U_stack (over m): when their few output tiles cannot occupy the
+// group, the inner dimension is cut into S parts whose partial products (S x Lp x K)
+// are summed afterwards.  S = 1: no split.  Bounded to TR_RSPLIT_MAX doubles.
+constexpr int64_t TR_RSPLIT_MAX = int64_t(1) << 23;
+HM_HD inline int32_t trunc_rsplit(int32_t m, int32_t q, int32_t cap, int32_t Ks, int32_t nsub) {
+    const int64_t Lp = (cap + TR_RB > TR_PW) ? cap + TR_RB : TR_PW;
+    int64_t s = nsub;
+    const int64_t by_mem = TR_RSPLIT_MAX / (Lp * (Ks > 0 ? Ks : 1));
+    const int64_t by_len = (m < q ? m : q) / 256;
+    if (by_mem < s) s = by_mem;
+    if (by_len < s) s = by_len;
+    return s < 2 ? 1 : (int32_t)s;
+}
 // split-K of the W = V_stack P product (partials nsub x q x L) only for small q
 constexpr int TR_WSPLIT_Q = 512;
 HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t cap, int32_t Ks, int32_t nsub) {
@@ -129,13 +143,15 @@ HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t
     const int64_t nch = (m + TR_RCH - 1) / TR_RCH + (q + TR_RCH - 1) / TR_RCH;
     TruncWs w;
     int64_t o = 0;
-    const int64_t sz[24] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_PW, (int64_t)m * Ks, (int64_t)q * Ks,
+    const int32_t rs = trunc_rsplit(m, q, cap, Ks, nsub);
+    const int64_t Lp = (L > TR_PW) ? L : TR_PW;
+    const int64_t sz[25] = {4 + (TR_LMAX + 16) / 2, (int64_t)q * TR_PW, (int64_t)m * Ks, (int64_t)q * Ks,
                             (int64_t)TR_PW * Ks, (int64_t)m * TR_PW, nch * TR_PW, (int64_t)m * L, L * TR_RB,
                             L * (int64_t)Ks, (int64_t)q * L, (int64_t)q * L, L * L, L * L, L * L, L * L, L, L,
                             ns * L * TR_RB, ns * L * TR_RB, ns * TR_RB * TR_RB, ns * L * L, ns * m * TR_PW,
-                            (q <= TR_WSPLIT_Q) ? ns * q * L : 0};
-    double* ptr[24];
-    for (int i = 0; i < 24; ++i) {
+                            (q <= TR_WSPLIT_Q) ? ns * q * L : 0, rs > 1 ? rs * Lp * Ks : 0};
+    double* ptr[25];
+    for (int i = 0; i < 25; ++i) {
         ptr[i] = base + o;
         o += (sz[i] + 7) & ~int64_t(7);
     }
@@ -143,6 +159,7 @@ HM_HD inline TruncWs trunc_ws_layout(double* base, int32_t m, int32_t q, int32_t
     w.npart = ptr[6]; w.Q = ptr[7]; w.Cb = ptr[8]; w.Pt = ptr[9]; w.Wm = ptr[10]; w.Wc = ptr[11];
     w.S = ptr[12]; w.Z = ptr[13]; w.Xo = ptr[14]; w.G = ptr[15]; w.tau = ptr[16]; w.sig = ptr[17];
     w.Cp = ptr[18]; w.Cf = ptr[19]; w.Gp = ptr[20]; w.Gp2 = ptr[21]; w.Ypart = ptr[22]; w.Wpart = ptr[23];
+    w.Rpart = ptr[24];
     w.total = o + 64;
     return w;
 }

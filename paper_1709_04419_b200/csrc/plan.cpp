@@ -528,6 +528,33 @@ struct Builder {
             return;
         }
         const int32_t s0 = C(s).child[0], s1 = C(s).child[1];
+        const BStore& so = P.bs[B(d).child[1]];
+        if (so.x_off >= 0) {
+            // two leaves: [V0; V1] <- [L00^{-1} 0; X10 L11^{-1}] [V0; V1] in one task per column
+            // chunk (V1 first: it reads the old V0)
+            const Thin V0 = sub(V, s0), V1 = sub(V, s1);
+            for (int32_t oc = 0; oc < V.cols; oc += 64) {
+                Prog pg;
+                zero(pg, 0, dstat(so.m), wdim(V, oc));
+                VIns lx = mk(VM_LD);
+                lx.t0 = 1; lx.rows = dstat(so.m); lx.cols = dstat(so.p); lx.goff = so.x_off; lx.ld = so.m;
+                pg.ins.push_back(lx);
+                pg.reads.push_back(so.x_res);
+                ld_thin(pg, 2, V0, s0, oc);
+                gemm(pg, 0, 1, false, 2, false, 1.0, 1.0);
+                ld_inv(pg, 1, P.diag_of[s1]);
+                ld_thin(pg, 2, V1, s1, oc);
+                gemm(pg, 0, 1, false, 2, false, 1.0, 1.0);
+                st_thin(pg, 0, V1, s1, oc);
+                zero(pg, 0, dstat((int32_t)C(s0).size()), wdim(V, oc));
+                ld_inv(pg, 1, P.diag_of[s0]);
+                ld_thin(pg, 2, V0, s0, oc);
+                gemm(pg, 0, 1, false, 2, false, 1.0, 1.0);
+                st_thin(pg, 0, V0, s0, oc);
+                emit_vm(pg);
+            }
+            return;
+        }
         fsolve(s0, sub(V, s0));
         hxt(B(d).child[1], sub(V, s0), sub(V, s1), -1.0, true);
         fsolve(s1, sub(V, s1));
@@ -778,6 +805,21 @@ struct Builder {
             trsm(off);
             pend[B(d).child[2]].prods.push_back({off, off});
             chol(t1);
+            if (P.bs[off].x_off >= 0) {
+                // X10 = -L11^{-1} L10 L00^{-1} for one-task forward solves over t (fsolve)
+                const BStore& so = P.bs[off];
+                Prog pg;
+                ld_inv(pg, 0, P.diag_of[t1]);
+                ld_dense(pg, 1, off);
+                gemm(pg, 2, 0, false, 1, false, 1.0, 0.0);
+                ld_inv(pg, 0, P.diag_of[t0]);
+                gemm(pg, 1, 2, false, 0, false, -1.0, 0.0);
+                VIns st = mk(VM_ST);
+                st.t0 = 1; st.rows = dstat(so.m); st.cols = dstat(so.p); st.goff = so.x_off; st.ld = so.m;
+                pg.ins.push_back(st);
+                pg.writes.push_back(so.x_res);
+                emit_vm(pg);
+            }
         } else {
             Prog pg;
             ld_dense(pg, 0, d);
@@ -991,6 +1033,17 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
             s.v_res0 = bld.new_res(P.leaf_count[bk.s]);
             P.bytes_C += 8LL * (s.m + s.p) * s.cap;
         }
+    }
+    // X10 blocks of the two-leaf diagonal clusters (see BStore::x_off)
+    for (int32_t c = 0; c < nc; ++c) {
+        const Cluster& cl = T.clusters[c];
+        if (cl.leaf() || !T.clusters[cl.child[0]].leaf() || !T.clusters[cl.child[1]].leaf()) continue;
+        const int32_t d = P.diag_of[c];
+        if (d < 0 || P.bs[d].kind != ST_SUB) continue;
+        BStore& o = P.bs[T.blocks[d].child[1]];
+        if (o.kind != ST_DENSE) continue;
+        o.x_off = bld.alloc((int64_t)o.m * o.p);
+        o.x_res = bld.new_res(1);
     }
     P.logd_off = bld.alloc(P.n_leaves);
     P.zw = 64;

@@ -27,6 +27,9 @@ struct BStore {
     int32_t u_res0 = -1, v_res0 = -1;  // first leaf-chunk resource of U (rows t) / V (rows s)
     int64_t inv_off = -1;        // diagonal leaf blocks: L^{-1} (m x m) written with the factor
     int32_t inv_res = -1;
+    int64_t x_off = -1;          // dense leaf block (c1, c0) of a two-leaf diagonal cluster c:
+    int32_t x_res = -1;          // X10 = -L11^{-1} L10 L00^{-1} (|c1| x |c0|), the off-diagonal
+                                 // block of L_cc^{-1}, so a forward solve over c is one task
 };
 
 // A matrix whose rows are the points of a cluster (tree order), split into

@@ -345,6 +345,42 @@ __device__ __forceinline__ void coop_sync(int* bar, int nsub, int& gen, unsigned
     }
 }
 
+// C (M x N, ldc) = op(A) op(B) with the inner dimension Kd cut into rs parts when the output
+// has fewer tiles (64 x 64) than the group has CTAs: units (part, tile) are spread over the
+// group, partials go to Rp (rs x ldp x N, ldp >= M), and each CTA then sums the columns
+// [c0, c1) it owns (the caller's slice) -- the caller synchronises before reading others'.
+// A and B are given at row offset 0 of the inner dimension (A: Kd x M transposed, B: Kd x N).
+__device__ __forceinline__ void gemm_tn_rsplit(int M, int N, int Kd, const double* A, int64_t lda, const double* B,
+                                               int64_t ldb, double* C, int64_t ldc, double* Rp, int64_t ldp, int rs,
+                                               int sub, int nsub, int c0, int c1, int* bar, int& gen,
+                                               unsigned long long* stt, double* gsm) {
+    const int tm = (M + 63) / 64, tn = (N + 63) / 64;
+    const int Kp = ((Kd + rs - 1) / rs + 15) & ~15;
+    for (int u = sub; u < rs * tm * tn; u += nsub) {
+        const int p = u / (tm * tn), tile = u % (tm * tn);
+        const int k0 = min(Kd, p * Kp), k1 = min(Kd, k0 + Kp);
+        double* Cp = Rp + (int64_t)p * ldp * N;
+        if (k1 > k0) {
+            gemm_wide(M, N, k1 - k0, 1.0, gop(A + k0, lda, true), gop(B + k0, ldb, false), 0.0, Cp, ldp, tile, tm * tn,
+                      gsm);
+        } else {
+            const int i0 = (tile % tm) * 64, j0 = (tile / tm) * 64;
+            for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+                const int i = i0 + (idx & 63), j = j0 + (idx >> 6);
+                if (i < M && j < N) Cp[i + (int64_t)j * ldp] = 0.0;
+            }
+        }
+    }
+    coop_sync(bar, nsub, gen, stt);
+    for (int idx = threadIdx.x; idx < M * (c1 - c0); idx += blockDim.x) {
+        const int i = idx % M, j = c0 + idx / M;
+        double a = 0.0;
+        for (int p = 0; p < rs; ++p) a += __ldcg(Rp + (int64_t)p * ldp * N + i + (int64_t)j * ldp);
+        C[i + (int64_t)j * ldc] = a;
+    }
+    __syncthreads();
+}
+
 // piece containing stacked column k (koff: prefix widths, np + 1 entries)
 __device__ __forceinline__ int piece_of(const int* koff, int np, int k) {
     int lo = 0, hi = np - 1;
@@ -525,6 +561,8 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     const int m = t.m, q = t.q, cap = t.cap, np = t.piece_count;
     const int L = cap + TR_RB;
     const int Ks = t.kmax_tot;
+    const int rsplit = (nsub == t.nsub) ? trunc_rsplit(m, q, cap, Ks, t.nsub) : 1;
+    const bool rowsplit = nsub > 1 && (m + TR_RCH - 1) / TR_RCH >= nsub;   // R3 over owned rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nchm = (m + TR_RCH - 1) / TR_RCH, nchq = (q + TR_RCH - 1) / TR_RCH;
     TruncWs W = trunc_ws_layout(pool + t.ws, m, q, cap, Ks, t.nsub);
@@ -609,27 +647,46 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             }
         }
         coop_sync(bar, nsub, gen, stt);            // Omega (and the gathered stacks) complete
-        // ---- R2: T^T = Omega^T V_stack  (TR_PW x K), one pass over the stack for all blocks
-        gemm_wide(TR_PW, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_PW, sub, nsub, gsm);
-        coop_sync(bar, nsub, gen, stt);
-        // ---- R3: Y = U_stack T  (m x TR_PW), split over the stacked columns (each CTA one
-        // 16-aligned slice, partials reduced on the owned 64-row chunks)
         {
             const int Kc = ((K + nsub - 1) / nsub + 15) & ~15;
             const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);
-            double* Yp = (nsub == 1) ? W.Y : W.Ypart + (int64_t)sub * m * TR_PW;
-            if (k1 > k0)
-                gemm_wide(m, TR_PW, k1 - k0, 1.0, gop(W.Ast + (int64_t)k0 * m, m, false),
-                          gop(W.Tt + (int64_t)k0 * TR_PW, TR_PW, true), 0.0, Yp, m, 0, 1, gsm);
-            else
-                for (int idx = threadIdx.x; idx < m * TR_PW; idx += blockDim.x) Yp[idx] = 0.0;
-            coop_sync(bar, nsub, gen, stt);
+            // ---- R2: T^T = Omega^T V_stack  (TR_PW x K), one pass over the stack for all blocks
+            // (few output tiles: inner dimension q split over the group, each CTA sums its own
+            // R3 slice of T)
+            if (rsplit > 1 && gemm_tiles(TR_PW, K, 64, 64) < nsub) {
+                gemm_tn_rsplit(TR_PW, K, q, W.Om, q, W.Bst, q, W.Tt, TR_PW, W.Rpart, TR_PW, rsplit, sub, nsub, k0, k1,
+                               bar, gen, stt, gsm);
+                if (rowsplit) coop_sync(bar, nsub, gen, stt);   // the row-split R3 reads all of T
+            } else {
+                gemm_wide(TR_PW, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_PW, sub, nsub, gsm);
+                coop_sync(bar, nsub, gen, stt);
+            }
+            // ---- R3: Y = U_stack T  (m x TR_PW), split over the stacked columns (each CTA one
+            // 16-aligned slice, partials reduced on the owned 64-row chunks)
+            // (tall blocks, at least one 64-row chunk per CTA: split over the owned row chunks
+            // instead -- no partial sums)
+            if (rowsplit) {
+                for (int c = sub; c < nchm; c += nsub) {
+                    const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
+                    gemm_wide(rows, TR_PW, K, 1.0, gop(W.Ast + r0, m, false), gop(W.Tt, TR_PW, true), 0.0, W.Y + r0, m,
+                              0, 1, gsm);
+                }
+                __syncthreads();
+            } else {
+                double* Yp = (nsub == 1) ? W.Y : W.Ypart + (int64_t)sub * m * TR_PW;
+                if (k1 > k0)
+                    gemm_wide(m, TR_PW, k1 - k0, 1.0, gop(W.Ast + (int64_t)k0 * m, m, false),
+                              gop(W.Tt + (int64_t)k0 * TR_PW, TR_PW, true), 0.0, Yp, m, 0, 1, gsm);
+                else
+                    for (int idx = threadIdx.x; idx < m * TR_PW; idx += blockDim.x) Yp[idx] = 0.0;
+                coop_sync(bar, nsub, gen, stt);
+            }
         }
         flops += 4.0 * TR_PW * (double)K * (m + q);
         bytes += 8.0 * Srows;
         for (int c = sub; c < nchm; c += nsub) {
             const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
-            if (nsub > 1) {
+            if (nsub > 1 && !rowsplit) {
                 for (int idx = threadIdx.x; idx < (r1 - r0) * TR_PW; idx += blockDim.x) {
                     const int64_t e = r0 + idx % (r1 - r0) + (int64_t)(idx / (r1 - r0)) * m;
                     double acc = 0.0;
@@ -777,8 +834,16 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         return;
     }
     // ---- F1: P^T = Q^T U_stack  (ell x K);  F2: W = V_stack P  (q x ell)
-    gemm_wide(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
-    coop_sync(bar, nsub, gen, stt);
+    if (rsplit > 1 && gemm_tiles(ell, K, 64, 64) < nsub) {
+        const int Kc = ((K + nsub - 1) / nsub + 15) & ~15;
+        const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);
+        gemm_tn_rsplit(ell, K, m, W.Q, m, W.Ast, m, W.Pt, L, W.Rpart, L, rsplit, sub, nsub, k0, k1, bar, gen, stt,
+                       gsm);
+        if (!(nsub > 1 && q <= TR_WSPLIT_Q)) coop_sync(bar, nsub, gen, stt);   // F2 below reads all of P
+    } else {
+        gemm_wide(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
+        coop_sync(bar, nsub, gen, stt);
+    }
     if (nsub > 1 && q <= TR_WSPLIT_Q) {            // split over the stacked columns, reduce owned rows
         const int Kc = ((K + nsub - 1) / nsub + 15) & ~15;
         const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);

@@ -18,4 +18,4 @@ H.trace(False, f"/tmp/trace_{which}.bin")
 T = hm.Tree(pts, leaf, 2.0)
 T.plan_dump(f"/tmp/plan_{which}.bin", 160)
 print(H.timings())
-print(analyse(f"/tmp/plan_{which}.bin", f"/tmp/trace_{which}.bin", "chol", grid=296))
+print(analyse(f"/tmp/plan_{which}.bin", f"/tmp/trace_{which}.bin", "chol", grid=148))

@@ -122,6 +122,26 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
         gaps = [claim[path[k + 1]] - end[path[k]] for k in range(len(path) - 1)]
         lines.append("  CP hand-over gap (claim of next - end of previous), us: mean %.2f median %.2f total %.1f ms"
                      % (np.mean(gaps), np.median(gaps), np.sum(np.maximum(gaps, 0)) / 1e3))
+        cta = (tr[:, 3] >> 32).astype(np.int64)
+        same = np.array([cta[path[k + 1]] == cta[path[k]] for k in range(len(path) - 1)])
+        g = np.array(gaps)
+        lines.append("    same CTA (continuation): %d of %d, gap total %.1f ms; other CTA: gap mean %.2f us, total %.1f ms,"
+                     " >20us: %d (total %.1f ms)" % (same.sum(), len(same), np.sum(np.maximum(g[same], 0)) / 1e3,
+                                                     g[~same].mean() if (~same).any() else 0,
+                                                     np.sum(np.maximum(g[~same], 0)) / 1e3, (g[~same] > 20).sum(),
+                                                     np.sum(g[~same][g[~same] > 20]) / 1e3))
+        big = [k for k in range(len(path) - 1) if gaps[k] > 20]
+        kinds = {}
+        for k in big:
+            key = ("trunc" if kind[path[k]] == 1 else "vm") + "->" + ("trunc" if kind[path[k + 1]] == 1 else "vm")
+            a = kinds.setdefault(key, [0, 0.0]); a[0] += 1; a[1] += gaps[k]
+        lines.append("    gaps > 20 us by (prev -> next) kind: " + ", ".join(f"{k}: {v[0]} / {v[1] / 1e3:.1f} ms" for k, v in kinds.items()))
+        # how busy was the machine when those CP tasks waited: tasks running at the ready instant
+        st_ = np.sort(claim); en_ = np.sort(end)
+        busy = [int(np.searchsorted(st_, end[path[k]]) - np.searchsorted(en_, end[path[k]])) for k in big[:2000]]
+        if busy:
+            lines.append("    running tasks when a >20 us-gap CP task became ready: mean %.0f, min %d, max %d (grid %d)"
+                         % (np.mean(busy), np.min(busy), np.max(busy), grid))
     lines.append("  critical-path MGEMM_ST tasks by terms (<=b: count, ms, mean us, mean terms):")
     for b in sorted(hist):
         c, d, nt = hist[b]
