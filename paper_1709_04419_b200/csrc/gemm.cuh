@@ -23,10 +23,10 @@ namespace hm {
 constexpr int GM_BK = 16;
 constexpr int GM_NS = 4;      // stages of the tile-VM products (staged in two 64 x 68 tiles)
 #ifndef HM_GM_NSC
-#define HM_GM_NSC 8
+#define HM_GM_NSC 4
 #endif
-constexpr int GM_NSC = HM_GM_NSC;   // stages of cta_gemm (truncations): with one CTA per SM
-                                    // the deeper pipeline keeps ~100 KB of loads in flight
+constexpr int GM_NSC = HM_GM_NSC;   // stages of cta_gemm (truncations); 8 measured slower at
+                                    // n = 64k (the truncation products are short: the ramp counts)
 
 struct GOp {
     const double* p;
