@@ -20,15 +20,18 @@ namespace {
 // rough task durations (microseconds on one CTA) for the bottom-level priority;
 // only their ratios matter (trace-calibrated, tools/trace_analyze.py)
 double vm_cost(const Phase& p, const VTask& v) {
-    double c = 2.0;
+    // measured at n = 64k (tools/trace_analyze.py): a one-term VM_MGEMM_ST task ~10 us,
+    // ~3 us per further term; tile loads ~1.5 us; POTRF + TRTRI ~20 us
+    double c = 6.0;
     for (int k = 0; k < v.ins_count; ++k) {
         const VIns& I = p.ins[v.ins_begin + k];
         switch (I.op) {
-            case VM_MGEMM: c += 2.0 * I.ld; break;
-            case VM_MGEMM_ST: c += 2.0 * I.t1; break;
-            case VM_POTRF: case VM_TRTRI: c += 6.0; break;
-            case VM_GEMM: case VM_TRSM_RLT: case VM_TRSM_LN: case VM_TRMM_LN: c += 2.0; break;
-            default: c += 0.7; break;
+            case VM_MGEMM: c += 1.0 + 3.0 * I.ld; break;
+            case VM_MGEMM_ST: c += 1.0 + 3.0 * I.t1; break;
+            case VM_POTRF: case VM_TRTRI: c += 10.0; break;
+            case VM_GEMM: case VM_TRSM_RLT: case VM_TRSM_LN: case VM_TRMM_LN: c += 4.0; break;
+            case VM_LD: c += 1.5; break;
+            default: c += 0.5; break;
         }
     }
     return c;

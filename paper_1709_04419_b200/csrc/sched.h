@@ -18,7 +18,7 @@
 
 namespace hm {
 
-constexpr int RQ_NSINGLE = 16;                 // priority levels for single tasks
+constexpr int RQ_NSINGLE = 28;                 // priority levels for single tasks
 constexpr int RQ_NCOOP = 4;                    // priority levels for cooperative groups
 constexpr int RQ_NQ = RQ_NSINGLE + RQ_NCOOP;   // queues, scanned 0 (highest) .. RQ_NQ-1
 static_assert(RQ_NQ <= 32, "one queue per lane of the scheduling warp");
