@@ -180,7 +180,7 @@ int hm_plan_dump(hm_tree t, int32_t kmax, const char* path, double summary[8]) {
                 std::fwrite(&size, 8, 1, f);
                 if (count) std::fwrite(p, (size_t)size, (size_t)count, f);
             };
-            int64_t hdr[8] = {P.pool_total, P.n_slots, P.logd_off, P.z_off, P.zw, t->T.n, P.n_leaves, 0};
+            int64_t hdr[8] = {P.pool_total, P.n_slots, P.logd_off, P.z_off, P.zw, t->T.n, P.n_leaves, P.z_slot};
             put(hdr, 8, 8);
             put(P.dgen.data(), (int64_t)P.dgen.size(), sizeof(DenseGenTask));
             put(P.aca.data(), (int64_t)P.aca.size(), sizeof(AcaTask));

@@ -238,6 +238,9 @@ void launch_scatter(const double* Zt, const int64_t* perm, int64_t n, int kz, do
     const int64_t tot = n * kz;
     k_scatter<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Zt, perm, n, kz, Z);
 }
+__global__ void k_set_int(int* p, int v) { *p = v; }
+void launch_set_int(int* p, int v, cudaStream_t st) { k_set_int<<<1, 1, 0, st>>>(p, v); }
+
 void launch_finish(const double* logd, int nleaves, const double* Zt, int64_t n, int kz, double* out,
                    cudaStream_t st) {
     k_finish<<<1, 512, 0, st>>>(logd, nleaves, Zt, n, kz, out);

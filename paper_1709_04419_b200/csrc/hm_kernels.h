@@ -29,6 +29,7 @@ void launch_exec_rq(const XTask* xr, int nx, const int32_t* succ2, const int32_t
                     unsigned long long* trace, int* bars, int nbars, cudaStream_t st);
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st);
 void launch_scatter(const double* Zt, const int64_t* perm, int64_t n, int kz, double* Z, cudaStream_t st);
+void launch_set_int(int* p, int v, cudaStream_t st);   // z-buffer column count -> its rank slot
 void launch_finish(const double* logd, int nleaves, const double* Zt, int64_t n, int kz, double* out,
                    cudaStream_t st);
 }  // namespace hm

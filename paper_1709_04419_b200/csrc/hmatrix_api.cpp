@@ -208,7 +208,8 @@ int max_rank(hm_handle_s* h) {
                                 h->stream));
     HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     int mx = 0;
-    for (int r : h->h_ranks) mx = std::max(mx, r);
+    for (int i = 0; i < h->P.n_slots; ++i)
+        if (i != h->P.z_slot) mx = std::max(mx, h->h_ranks[i]);   // z_slot: RHS width, not a rank
     return mx;
 }
 
@@ -279,6 +280,10 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
         {
             Launch L(h, KF_AUX);
             launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+        }
+        {
+            Launch L(h, KF_AUX);   // the solve's tile products cover only the kc active columns
+            launch_set_int(h->ranks.as<int>() + h->P.z_slot, kc, h->stream);
         }
         run_phase(h, h->solve);
         {
@@ -463,6 +468,7 @@ int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k, do
                 src = h->zio.as<double>();
             }
             launch_gather(src, h->perm.as<int64_t>(), n, kc, zw, zt, h->stream);
+            launch_set_int(h->ranks.as<int>() + h->P.z_slot, kc, h->stream);
             run_phase(h, h->lmul);
             if (z_on_device) {
                 launch_scatter(zt, h->perm.as<int64_t>(), n, kc, Z + (int64_t)c0 * n, h->stream);

@@ -1048,6 +1048,7 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
     P.logd_off = bld.alloc(P.n_leaves);
     P.zw = 64;
     P.z_off = bld.alloc((int64_t)T.n * P.zw);
+    P.z_slot = P.n_slots++;
     const int32_t z_res0 = bld.new_res(P.n_leaves);
     P.pool_blocks = bld.bump;
     // temporary 64 x 64 tiles for split dense updates (see apply_dense_pending)
@@ -1107,7 +1108,7 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
         if (!pd.prods.empty() || !pd.pieces.empty()) throw std::logic_error("planner: unapplied pending update");
     // forward solve and sampler on the z buffer (rows = root cluster, tree order)
     Thin Z;
-    Z.off = P.z_off; Z.ld = (int32_t)T.n; Z.cluster = 0; Z.cols = P.zw; Z.slot = -1; Z.res0 = z_res0;
+    Z.off = P.z_off; Z.ld = (int32_t)T.n; Z.cluster = 0; Z.cols = P.zw; Z.slot = P.z_slot; Z.res0 = z_res0;
     bld.begin_phase(P.solve);
     bld.fsolve(0, Z);
     bld.end_phase();

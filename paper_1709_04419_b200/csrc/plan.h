@@ -73,6 +73,8 @@ struct Plan {
     int64_t logd_off = 0;              // n_leaves doubles
     int64_t z_off = 0;                 // solve RHS buffer: n x ZW (col-major, ld n)
     int32_t zw = 64;
+    int32_t z_slot = -1;               // rank slot holding the active column count of the z buffer
+                                       // (set by hm_loglik / hm_sample before the phase runs)
     int64_t bytes_C = 0;               // bytes of block storage at capacity
     int64_t ring_off = 0, ring_size = 0;  // truncation workspace ring (doubles)
     int64_t tmp_off = 0;                  // ring of 64 x 64 temporary tiles (split dense updates)

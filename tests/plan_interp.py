@@ -80,7 +80,8 @@ class Plan:
     def __init__(self, path):
         secs = _read(path)
         hdr = np.frombuffer(secs[0][2], "<i8", 8)
-        (self.pool_total, self.n_slots, self.logd_off, self.z_off, self.zw, self.n, self.n_leaves, _) = map(int, hdr)
+        (self.pool_total, self.n_slots, self.logd_off, self.z_off, self.zw, self.n, self.n_leaves,
+         self.z_slot) = map(int, hdr)
         assert secs[1][1] == DGEN.itemsize and secs[2][1] == ACA.itemsize
         self.dgen = np.frombuffer(secs[1][2], DGEN, secs[1][0])
         self.aca = np.frombuffer(secs[2][2], ACA, secs[2][0])
@@ -306,6 +307,7 @@ class Interp:
         buf = np.zeros((n, zw))
         buf[:, :k] = Z_tree
         self.pool[self.P.z_off:self.P.z_off + n * zw] = buf.ravel(order="F")
+        self.ranks[self.P.z_slot] = k            # active columns of the z buffer (hm_loglik)
         self.run(self.P.solve)
         v = self.pool[self.P.z_off:self.P.z_off + n * zw].reshape(zw, n).T[:, :k]
         logdet = 2.0 * float(np.sum(self.pool[self.P.logd_off:self.P.logd_off + self.P.n_leaves]))
@@ -319,6 +321,7 @@ class Interp:
         buf = np.zeros((n, zw))
         buf[:, :k] = X_tree
         self.pool[self.P.z_off:self.P.z_off + n * zw] = buf.ravel(order="F")
+        self.ranks[self.P.z_slot] = k
         self.run(self.P.lmul)
         return self.pool[self.P.z_off:self.P.z_off + n * zw].reshape(zw, n).T[:, :k].copy()
 
