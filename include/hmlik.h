@@ -62,13 +62,15 @@ typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
  * the scale of C), or relative to the block's norm when rel_eps = 1;
  * leaf: n_min (l.211); eta: admissibility parameter (reading R2); kmax: rank
  * capacity of one low-rank block, at most 240 (HM_ERR_RANK_CAP when exceeded;
- * 0 = default 160).                                                          */
+ * 0 = default 160); coop_max: most CTAs cooperating on one truncation (1..32,
+ * 0 = default 16; 8 when several handles share the GPU, see hm_set_exec_grid).  */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
     double  eta;
     int32_t kmax;
     int32_t rel_eps;
+    int32_t coop_max;
 } hm_params;
 
 typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */
@@ -167,6 +169,14 @@ int hm_profile(hm_handle h, int32_t enable);
  * Same task DAG and arithmetic; a cooperative truncation sums its partials in
  * a fixed order, so all modes agree to rounding.  HM_ERR_ARG for another mode. */
 int hm_set_exec_mode(hm_handle h, int32_t mode);
+
+/* Co-scheduling: cap the persistent executor of this handle at `ctas` CTAs (one
+ * per SM; 0 = all SMs).  Two handles with caps summing to the SM count, driven
+ * from two host threads on two streams, run their factorisations side by side
+ * (independent theta, e.g. a likelihood grid or Monte-Carlo replicates).  The
+ * cap must exceed 4 * (largest cooperative truncation group - 1) of the plan,
+ * else the next phase launch fails with HM_ERR_ARG.                           */
+int hm_set_exec_grid(hm_handle h, int32_t ctas);
 
 /* Diagnostics: hm_trace(h, 1, NULL) makes the persistent executor record, for
  * every task of each subsequent phase launch, (claim, dependencies-satisfied,

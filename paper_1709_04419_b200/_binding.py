@@ -31,7 +31,7 @@ class Theta(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32),
-                ("rel_eps", C.c_int32)]
+                ("rel_eps", C.c_int32), ("coop_max", C.c_int32)]
 
 
 def _load():
@@ -62,6 +62,7 @@ def _load():
         "hm_profile": ([P, I32], C.c_int),
         "hm_kernel_stats": ([P, P], C.c_int),
         "hm_set_exec_mode": ([P, I32], C.c_int),
+        "hm_set_exec_grid": ([P, I32], C.c_int),
         "hm_trace": ([P, I32, C.c_char_p], C.c_int),
         "hm_checksum": ([P, P], C.c_int),
         "hm_dense_loglik": ([P, I32, I64, Theta, P, I32, I32, I32, P, P], C.c_int),
@@ -78,7 +79,7 @@ lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
             "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_stats", "hm_timings", "hm_profile",
-            "hm_kernel_stats", "hm_set_exec_mode", "hm_trace", "hm_checksum",
+            "hm_kernel_stats", "hm_set_exec_mode", "hm_set_exec_grid", "hm_trace", "hm_checksum",
             "hm_dense_loglik", "hm_matern_block")
 
 
@@ -202,13 +203,13 @@ class HMatrix:
     """
 
     def __init__(self, locs, theta, eps: float = 1e-8, leaf: int = 32, eta: float = 2.0, kmax: int = 160,
-                 device: int = 0, stream=None, rel_eps: bool = False):
+                 device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0):
         if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
             locs = _as_f64(locs)
         lp, ld = ptr_of(locs)
         self.n = int(locs.shape[0])
         self._h = C.c_void_p()
-        self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0)
+        self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0, int(coop_max))
         rc = lib.hm_build(lp, ld, self.n, Theta(*theta), self.params, int(device),
                           C.c_void_p(stream) if stream else None, C.byref(self._h))
         check(rc)
@@ -257,6 +258,11 @@ class HMatrix:
         check(lib.hm_profile(self._h, 1 if enable else 0))
 
     KERNEL_FAMILIES = ("k_dense_gen", "k_aca", "k_trunc", "k_vm", "k_aux", "k_exec")
+
+    def set_exec_grid(self, ctas: int):
+        """Cap this handle's persistent executor at `ctas` CTAs (0 = all SMs), so
+        several handles can run side by side on different streams."""
+        check(lib.hm_set_exec_grid(self._h, int(ctas)))
 
     def set_exec_mode(self, mode: int):
         """2 = persistent ready-queue executor (default), 1 = persistent topological-claim

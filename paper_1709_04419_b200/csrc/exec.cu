@@ -288,10 +288,12 @@ void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, 
 void launch_exec_rq(const XTask* xr, int nx, const int32_t* succ2, const int32_t* qbase, const int32_t* slot_init, const int32_t* ctl_init,
                     int* cnt, int* slot, int* ctl, const VTask* vt, const VIns* ins, const VTerm* terms, const TTask* tt,
                     const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps,
-                    unsigned long long* trace, int* bars, int nbars, cudaStream_t st) {
+                    unsigned long long* trace, int* bars, int nbars, int max_nsub, int grid_cap, cudaStream_t st) {
     if (nx <= 0) return;
-    const int grid = exec_grid_rq();
-    if (grid <= RQ_NCOOP * (TR_COOP_MAX - 1)) throw ApiError(HM_ERR_ARG, "ready-queue executor needs more resident CTAs");
+    int grid = exec_grid_rq();
+    if (grid_cap > 0 && grid_cap < grid) grid = grid_cap;
+    // deadlock freedom: CTAs blocked in partially claimed groups (<= RQ_NCOOP groups) < grid
+    if (grid <= RQ_NCOOP * (max_nsub - 1)) throw ApiError(HM_ERR_ARG, "ready-queue executor needs more resident CTAs");
     HM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * nx, st));
     HM_CUDA_TRY(cudaMemcpyAsync(slot, slot_init, sizeof(int) * nx, cudaMemcpyDeviceToDevice, st));
     HM_CUDA_TRY(cudaMemcpyAsync(ctl, ctl_init, sizeof(int) * (2 * RQ_NQ + 2), cudaMemcpyDeviceToDevice, st));

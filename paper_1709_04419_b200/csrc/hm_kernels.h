@@ -26,7 +26,7 @@ void launch_exec(const XTask* xt, int nx, const int32_t* deps, const VTask* vt, 
 void launch_exec_rq(const XTask* xr, int nx, const int32_t* succ2, const int32_t* qbase, const int32_t* slot_init, const int32_t* ctl_init,
                     int* cnt, int* slot, int* ctl, const VTask* vt, const VIns* ins, const VTerm* terms, const TTask* tt,
                     const TPiece* tp, double* pool, int* ranks, int* flags, double* ctr, double eps,
-                    unsigned long long* trace, int* bars, int nbars, cudaStream_t st);
+                    unsigned long long* trace, int* bars, int nbars, int max_nsub, int grid_cap, cudaStream_t st);
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st);
 void launch_scatter(const double* Zt, const int64_t* perm, int64_t n, int kz, double* Z, cudaStream_t st);
 void launch_set_int(int* p, int v, cudaStream_t st);   // z-buffer column count -> its rank slot

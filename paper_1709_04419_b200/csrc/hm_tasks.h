@@ -114,7 +114,9 @@ constexpr int TR_PMAX = 1023;     // pieces per truncation
 #define HM_COOP_WORK_LOG2 17
 #endif
 constexpr int64_t TR_COOP_WORK = int64_t(1) << HM_COOP_WORK_LOG2;   // (m + q) * static K per cooperating CTA
-constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation
+constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation (hard limit; the plan's
+                                  // cap hm_params.coop_max defaults to TR_COOP_DEFAULT)
+constexpr int TR_COOP_DEFAULT = 16;
 
 struct TruncWs {                  // randomized-path workspace (doubles unless noted)
     double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp,
@@ -170,7 +172,7 @@ inline int64_t trunc_ws_size(int32_t m, int32_t q, int32_t cap, int32_t kmax_tot
     }
     return trunc_ws_layout(nullptr, m, q, cap, kmax_tot, nsub).total;
 }
-inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
+inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot, int32_t cap = TR_COOP_DEFAULT) {
     if (trunc_exact_path(m, q, kmax_tot)) return 1;
     // one CTA per TR_COOP_WORK of stacked data, at most two per 64-row chunk of the
     // larger side (a group must assemble before it starts: more CTAs than rows to
@@ -180,6 +182,7 @@ inline int32_t trunc_nsub(int32_t m, int32_t q, int32_t kmax_tot) {
     const int64_t gmax = HM_COOP_ROWFAC * ((rows + TR_RCH - 1) / TR_RCH);
     int64_t n = g < 1 ? 1 : g;
     if (n > gmax) n = gmax;
+    if (n > cap) n = cap;
     if (n > TR_COOP_MAX) n = TR_COOP_MAX;
     return (int32_t)n;
 }

@@ -65,6 +65,7 @@ Dim ddyn(int32_t stat, int32_t slot, int32_t off) { return Dim{stat, slot, off, 
 struct Builder {
     const Tree& T;
     Plan& P;
+    int32_t coop_max = TR_COOP_DEFAULT;   // cap of cooperative truncation groups (hm_params.coop_max)
     int64_t bump = 0;
     int32_t nres = 0;
     std::vector<int32_t> lw_wave, rd_wave;
@@ -762,7 +763,7 @@ struct Builder {
             kt0 += p.w.stat;
             wmax0 = std::max(wmax0, p.w.stat);
         }
-        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, trunc_nsub(s.m, s.p, kt0));
+        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, trunc_nsub(s.m, s.p, kt0, coop_max));
         const int64_t nch = (wsz + ring_chunk - 1) / ring_chunk;
         if (4 * nch > ring_nchunks) grow_ring(4 * nch);   // keep >= 4 workspaces of this size in flight
         if (ring_ptr + nch > ring_nchunks) ring_ptr = 0;
@@ -786,7 +787,7 @@ struct Builder {
         t.ws_size = wsz;
         t.ws = ws_off;
         if ((int32_t)pcs.size() > TR_PMAX) throw std::logic_error("truncation with more than TR_PMAX pieces");
-        t.nsub = trunc_nsub(s.m, s.p, kt);
+        t.nsub = trunc_nsub(s.m, s.p, kt, coop_max);
         t.bar = t.nsub > 1 ? ph->n_bars++ : 0;
         ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
         xraw.push_back({w, 1, (int32_t)traw.size(), std::move(deps)});
@@ -963,7 +964,7 @@ std::string Plan::summary() const {
     return buf;
 }
 
-void build_plan(const Tree& T, int32_t kmax, Plan& P) {
+void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max) {
     if (T.leaf > 64) throw std::invalid_argument("leaf size > 64 is not supported by the tile VM");
     P = Plan();
     P.kmax = kmax;
@@ -999,6 +1000,8 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
         for (int32_t c = 0; c < nc; ++c) P.leaf_begin[c] = first[c];
     }
     Builder bld(T, P);
+    if (coop_max < 1 || coop_max > TR_COOP_MAX) throw std::invalid_argument("coop_max must be in [1, 32]");
+    bld.coop_max = coop_max;
     // block storage
     const int32_t nb = (int32_t)T.blocks.size();
     P.bs.assign(nb, BStore());
@@ -1068,7 +1071,7 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P) {
             const BStore& s = P.bs[b];
             if (s.kind != ST_LR) continue;
             lr_order.push_back(b);
-            const int64_t w = trunc_ws_size(s.m, s.p, s.cap, s.cap, trunc_nsub(s.m, s.p, s.cap));
+            const int64_t w = trunc_ws_size(s.m, s.p, s.cap, s.cap, trunc_nsub(s.m, s.p, s.cap, coop_max));
             maxs = std::max(maxs, w);
             sum += w;
             maxs = std::max(maxs, trunc_ws_size(s.m, s.p, s.cap, TR_EXACT_K + 1, 1));

@@ -92,6 +92,6 @@ struct Plan {
 
 // Build the full plan for a tree.  Throws std::invalid_argument for
 // unsupported geometry (leaf > 64, leaves at different depths).
-void build_plan(const Tree& T, int32_t kmax, Plan& P);
+void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max = TR_COOP_DEFAULT);
 
 }  // namespace hm

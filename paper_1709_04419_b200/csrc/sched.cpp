@@ -122,6 +122,8 @@ void build_sched(const Phase& p, Sched& s) {
         s.ctl_init[2 * q] = 0;
         s.ctl_init[2 * q + 1] = tail[q];
     }
+    s.max_nsub = 1;
+    for (int i = 0; i < nx; ++i) s.max_nsub = std::max(s.max_nsub, p.xt[i].nsub);
     s.succ2.resize(2 * s.succ.size());
     for (size_t k = 0; k < s.succ.size(); ++k) {
         const int v = s.succ[k];

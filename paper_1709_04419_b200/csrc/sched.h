@@ -31,6 +31,7 @@ struct Sched {
     std::vector<int32_t> qbase;        // RQ_NQ + 1: first slot of each queue
     std::vector<int32_t> slot_init;    // nx: task id in the slot (roots pre-filled) or -1
     std::vector<int32_t> ctl_init;     // 2 * RQ_NQ + 2: {head, tail} per queue, finished, pad
+    int32_t max_nsub = 1;              // largest cooperative group of the phase
     std::vector<int32_t> succ2;        // 2 |succ|: {successor, need << 11 | nsub << 5 | queue} (device form)
 };
 

@@ -177,3 +177,46 @@ def test_mc_mle_small(hm):
     H.cholesky()
     ll0 = H.loglik(Z)[0, 0]
     assert res[0, 3] >= ll0
+
+
+def test_coscheduled_handles_match_single(hm):
+    """Two handles co-scheduled on two streams from two host threads, each capped at
+    half the SMs (hm_set_exec_grid, coop_max 8), give bit-identical likelihoods to the
+    same evaluations run one at a time on the whole GPU: the executor's grid never
+    changes the arithmetic (the work split of a truncation is fixed by the plan)."""
+    import threading
+    import torch
+    pts = uniform_iid(16384, 5)
+    Z = standard_normal(16384, 1, 6)
+    ths = [(1.0, 0.05, 0.5), (1.3, 0.08, 1.0), (0.9, 0.03, 0.7), (1.1, 0.06, 1.4)]
+    H = hm.HMatrix(pts, ths[0], eps=1e-7, leaf=32, coop_max=8)
+    ref = []
+    for th in ths:
+        H.assemble(th)
+        H.cholesky()
+        ref.append(H.loglik(Z)[0, 0])
+    H.close()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    Hs = [hm.HMatrix(pts, ths[0], eps=1e-7, leaf=32, coop_max=8, stream=s.cuda_stream) for s in streams]
+    Hs[0].set_exec_grid(sms // 2)
+    Hs[1].set_exec_grid(sms - sms // 2)
+    got = [[], []]
+
+    def work(i):
+        for th in ths[i::2]:
+            Hs[i].assemble(th)
+            Hs[i].cholesky()
+            got[i].append(Hs[i].loglik(Z)[0, 0])
+
+    t = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for x in t:
+        x.start()
+    for x in t:
+        x.join()
+    assert got[0] == [ref[0], ref[2]] and got[1] == [ref[1], ref[3]]
+    with pytest.raises(hm.HMError):         # a cap below the deadlock bound is refused
+        Hs[0].set_exec_grid(2)
+        Hs[0].cholesky()
+    for x in Hs:
+        x.close()

@@ -1,0 +1,5 @@
+for ns in 4 8; do
+rm -rf paper_1709_04419_b200/build; HM_BUILD_DEFS="-DHM_GM_NSC=$ns" python paper_1709_04419_b200/build.py > /dev/null
+echo "NSC=$ns"; timeout 300 python tools/hm_trace_probe.py 64k 2>&1 | grep -A4 "makespan" | head -5
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | cut -c1-200
+done

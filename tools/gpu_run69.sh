@@ -1,0 +1,2 @@
+python paper_1709_04419_b200/build.py > /dev/null
+timeout 300 python tools/hm_trace_probe.py 64k > gpurun_out/trace64k_rq.txt 2>&1; grep -A18 "makespan" gpurun_out/trace64k_rq.txt | head -19

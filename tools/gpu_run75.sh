@@ -1,0 +1,4 @@
+python paper_1709_04419_b200/build.py > /dev/null
+timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --theta-streams 2 2>&1 | cut -c1-120
+timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --theta-streams 3 2>&1 | cut -c1-120
+timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --theta-streams 3 --no-profile 2>&1 | cut -c1-120

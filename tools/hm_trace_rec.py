@@ -14,11 +14,11 @@ H.trace(True)
 H.assemble(theta)
 H.trace(False, "/tmp/trace_rec.bin")
 print(H.timings())
-print(analyse("/tmp/plan_64k.bin", "/tmp/trace_rec.bin", "recompress", grid=296, top=8))
+print(analyse("/tmp/plan_64k.bin", "/tmp/trace_rec.bin", "recompress", grid=148, top=8))
 H.cholesky()
 Z = standard_normal(len(pts), 1, 3)
 H.trace(True)
 H.loglik(Z)
 H.trace(False, "/tmp/trace_sol.bin")
 print(H.timings())
-print(analyse("/tmp/plan_64k.bin", "/tmp/trace_sol.bin", "solve", grid=296, top=8))
+print(analyse("/tmp/plan_64k.bin", "/tmp/trace_sol.bin", "solve", grid=148, top=8))

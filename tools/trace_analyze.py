@@ -37,6 +37,17 @@ def analyse(plan_path: str, trace_path: str, phase: str = "chol", grid: int = 29
         lines.append(f"  {nm:6s} n={sel.sum():8d} busy={dur[sel].sum() / 1e3:10.3f} ms  mean={dur[sel].mean() if sel.any() else 0:8.2f} us"
                      f"  max={dur[sel].max() if sel.any() else 0:9.1f} us  dep-wait={wait[sel].sum() / 1e3:9.3f} ms")
     lines.append(f"  utilisation (busy / (makespan * grid)) = {dur.sum() / (mk * grid):.3f}")
+    # truncation busy time by class (m, q, nsub) and by actual stacked width
+    tsel = np.nonzero(kind == 1)[0]
+    if tsel.size:
+        cls = {}
+        for i in tsel:
+            t = ph.tt[ph.xt[i]["idx"]]
+            key = (int(t["m"]), int(t["q"]), int(ph.xt[i]["nsub"]), "exact" if int(t["kmax_tot"]) <= 160 and int(t["m"]) <= 512 and int(t["q"]) <= 512 else "rand")
+            c = cls.setdefault(key, [0, 0.0]); c[0] += 1; c[1] += dur[i]
+        lines.append("  truncation busy by (m, q, nsub, path): CTA-tasks, CTA-ms")
+        for k, (c, d) in sorted(cls.items(), key=lambda kv: -kv[1][1])[:12]:
+            lines.append(f"    {str(k):32s} {c:7d} {d / 1e3:10.1f}")
     # critical path with measured durations
     cp = np.zeros(n)
     arg = np.full(n, -1)
