@@ -227,10 +227,13 @@ def run_mc(args, w):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     from paper_1709_04419_b200.mle import mc_mle
-    reps = ws * (args.warmup + args.steps)
-    # warm-up replicates (untimed), then args.steps replicates per rank, timed
-    mc_mle(w["n"], ws * args.warmup, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"], leaf=w["leaf"],
-           rank=rk, world=ws, device=lr, seed=10_000, gather=False)
+    S = max(1, args.theta_streams)
+    sms = torch.cuda.get_device_properties(lr).multi_processor_count
+    strs = [torch.cuda.Stream(device=lr) for _ in range(S)] if S > 1 else None
+    handles = [x.cuda_stream for x in strs] if strs else None
+    # warm-up replicates (untimed), then args.steps * S replicates per rank, timed (S co-scheduled)
+    mc_mle(w["n"], ws * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"], leaf=w["leaf"],
+           rank=rk, world=ws, device=lr, seed=10_000, gather=False, streams=handles, sms=sms)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -238,8 +241,9 @@ def run_mc(args, w):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(lr) as clk:
         e0.record(stream)
-        res = mc_mle(w["n"], ws * args.steps, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
-                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False)
+        res = mc_mle(w["n"], ws * args.steps * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
+                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False, streams=handles, sms=sms)
+        torch.cuda.synchronize()
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -248,14 +252,14 @@ def run_mc(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     if rk == 0:
-        n_evals = ws * args.steps * w["evals"]
+        n_evals = ws * args.steps * S * w["evals"]
         line = {"metric": f"H-log-likelihood evals/sec (MC-MLE, n={w['n']})", "value": n_evals / (ms / 1e3),
                 "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{w['cfg']}: {w['evals']} Nelder-Mead evals per replicate, one replicate per "
-                                       f"rank per step (incl. its H-build and sampler), n={w['n']}, eps={w['eps']}",
-                           "parallelism": f"replicas x{ws}"},
+                "config": {"workload": f"{w['cfg']}: {w['evals']} Nelder-Mead evals per replicate, {S} replicate(s) per "
+                                       f"rank per step (incl. their H-build and sampler), n={w['n']}, eps={w['eps']}",
+                           "parallelism": f"replicas x{ws}; {S} co-scheduled replicates per GPU"},
                 "estimates_rank0": res.tolist(), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if dist:

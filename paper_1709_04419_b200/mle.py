@@ -99,25 +99,66 @@ def mle_replicate(H, Z, theta0, evals: int = 60, step: float = 0.3):
 
 
 def mc_mle(n: int, replicates: int, theta_true, theta0, eps: float = 1e-6, evals: int = 60, leaf: int = 32,
-           eta: float = 2.0, rank: int = 0, world: int = 1, device: int = 0, seed: int = 0, gather: bool = True):
+           eta: float = 2.0, rank: int = 0, world: int = 1, device: int = 0, seed: int = 0, gather: bool = True,
+           streams=None, sms: int = 0):
     """configs[3]: `replicates` independent data sets (n uniform iid locations in
     [0,1]^2, Z = L~(theta_true) xi drawn by the library's H-sampler at eps/100),
     each fitted by `evals` Nelder-Mead evaluations.  Replicates are sharded
-    round-robin over ranks; returns (replicates x 5): sigma2, ell, nu, loglik, evals."""
+    round-robin over ranks; returns (replicates x 5): sigma2, ell, nu, loglik, evals.
+
+    streams: optional list of S CUDA stream handles; the rank's replicates are then
+    co-scheduled on the GPU, S at a time (one host thread, stream and handle each,
+    executor capped at sms / S CTAs, cooperative truncations of <= 8 CTAs --
+    hm_set_exec_grid); results are identical to the sequential run."""
+    import threading
+
     from ._binding import HMatrix
     from synthetic import standard_normal, uniform_iid
 
-    out = []
-    for r in shard_indices(replicates, rank, world):
+    mine = list(shard_indices(replicates, rank, world))
+    S = len(streams) if streams else 1
+    res = {}
+
+    def fit(r, stream, cap):
+        kw = dict(leaf=leaf, eta=eta, device=device)
+        if stream is not None:
+            kw.update(stream=stream, coop_max=8)
         pts = uniform_iid(n, seed + 1000 * int(r))
-        Hs = HMatrix(pts, theta_true, eps=min(eps, 1e-8), leaf=leaf, eta=eta, device=device)
+        Hs = HMatrix(pts, theta_true, eps=min(eps, 1e-8), **kw)
+        if cap:
+            Hs.set_exec_grid(cap)
         Hs.cholesky()
         Z = Hs.sample(standard_normal(n, 1, seed + 1000 * int(r) + 1))[:, 0]
         Hs.close()
-        H = HMatrix(pts, theta0, eps=eps, leaf=leaf, eta=eta, device=device)
+        H = HMatrix(pts, theta0, eps=eps, **kw)
+        if cap:
+            H.set_exec_grid(cap)
         th, ll, ne = mle_replicate(H, Z, theta0, evals=evals)
         H.close()
-        out.append([th[0], th[1], th[2], ll, ne])
+        res[r] = [th[0], th[1], th[2], ll, ne]
+
+    if S <= 1:
+        for r in mine:
+            fit(r, None, 0)
+    else:
+        caps = [sms // S + (1 if i < sms % S else 0) for i in range(S)]
+        errs = []
+
+        def worker(i):
+            try:
+                for r in mine[i::S]:
+                    fit(r, streams[i], caps[i])
+            except Exception as e:  # surfaced after the join
+                errs.append(e)
+
+        th = [threading.Thread(target=worker, args=(i,)) for i in range(S)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+    out = [res[r] for r in mine]
     local = np.asarray(out, dtype=np.float64).reshape(-1, 5)
     if world > 1 and gather:
         return gather_results(local, replicates, rank, world)
