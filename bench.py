@@ -233,7 +233,7 @@ def run_mc(args, w):
     handles = [x.cuda_stream for x in strs] if strs else None
     # warm-up replicates (untimed), then args.steps * S replicates per rank, timed (S co-scheduled)
     mc_mle(w["n"], ws * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"], leaf=w["leaf"],
-           rank=rk, world=ws, device=lr, seed=10_000, gather=False, streams=handles, sms=sms)
+           rank=rk, world=ws, device=lr, seed=10_000, gather=False, streams=handles, sms=sms, kmax=args.kmax)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -242,7 +242,8 @@ def run_mc(args, w):
     with ClockSampler(lr) as clk:
         e0.record(stream)
         res = mc_mle(w["n"], ws * args.steps * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
-                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False, streams=handles, sms=sms)
+                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False, streams=handles, sms=sms,
+                     kmax=args.kmax)
         torch.cuda.synchronize()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -375,7 +376,7 @@ def run_gpu(args, w):
                 "n_gpus": ws, "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{w['cfg']}: n={n} {w['kind']}, theta={w['thetas']} (ell swept +-2%),"
-                                       f" leaf={w['leaf']}, eta={w['eta']}, eps={w['eps']}",
+                                       f" leaf={w['leaf']}, eta={w['eta']}, eps={w['eps']}, kmax={args.kmax}",
                            "l2": "no flush: H-matrix storage > 126 MB L2",
                            "parallelism": f"replicas x{ws}; {S} co-scheduled theta streams per GPU "
                                           f"(executor CTAs {caps if S > 1 else sms}, coop_max {coop}); "
@@ -433,7 +434,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hm", choices=["hm", "reference"])
     ap.add_argument("--workload", default="n64k", choices=sorted(WORKLOADS))
-    ap.add_argument("--kmax", type=int, default=160)
+    ap.add_argument("--kmax", type=int, default=64,
+                    help="rank capacity per low-rank block (ranks at the workloads' eps stay <= 30; HM_ERR_RANK_CAP if exceeded)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch CUDA events (kernel table empty)")
     ap.add_argument("--theta-streams", type=int, default=4,

@@ -100,7 +100,7 @@ def mle_replicate(H, Z, theta0, evals: int = 60, step: float = 0.3):
 
 def mc_mle(n: int, replicates: int, theta_true, theta0, eps: float = 1e-6, evals: int = 60, leaf: int = 32,
            eta: float = 2.0, rank: int = 0, world: int = 1, device: int = 0, seed: int = 0, gather: bool = True,
-           streams=None, sms: int = 0):
+           streams=None, sms: int = 0, kmax: int = 0):
     """configs[3]: `replicates` independent data sets (n uniform iid locations in
     [0,1]^2, Z = L~(theta_true) xi drawn by the library's H-sampler at eps/100),
     each fitted by `evals` Nelder-Mead evaluations.  Replicates are sharded
@@ -120,7 +120,7 @@ def mc_mle(n: int, replicates: int, theta_true, theta0, eps: float = 1e-6, evals
     res = {}
 
     def fit(r, stream, cap):
-        kw = dict(leaf=leaf, eta=eta, device=device)
+        kw = dict(leaf=leaf, eta=eta, device=device, kmax=kmax)
         if stream is not None:
             kw.update(stream=stream, coop_max=8)
         pts = uniform_iid(n, seed + 1000 * int(r))
