@@ -74,7 +74,15 @@ struct hm_handle_s {
     double ms[3] = {0, 0, 0};
     int max_rank_C = 0, max_rank_L = 0;
     std::vector<int> h_ranks;
+    // pinned host staging for host-buffer calls (pageable copies would serialise
+    // co-scheduled handles' streams)
+    double* pin_z = nullptr;
+    size_t pin_z_n = 0;
+    double* pin_out = nullptr;
+    size_t pin_out_n = 0;
     ~hm_handle_s() {
+        if (pin_z) cudaFreeHost(pin_z);
+        if (pin_out) cudaFreeHost(pin_out);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto& e : evpool)
@@ -268,6 +276,18 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
     const int64_t n = h->T.n;
     const int zw = h->P.zw;
     double* zt = h->pool.as<double>() + h->P.z_off;
+    if ((size_t)3 * k > h->pin_out_n) {
+        if (h->pin_out) HM_CUDA_TRY(cudaFreeHost(h->pin_out));
+        h->pin_out = nullptr;
+        HM_CUDA_TRY(cudaMallocHost(&h->pin_out, sizeof(double) * 3 * k));
+        h->pin_out_n = (size_t)3 * k;
+    }
+    if (!zdev && (size_t)n * zw > h->pin_z_n) {
+        if (h->pin_z) HM_CUDA_TRY(cudaFreeHost(h->pin_z));
+        h->pin_z = nullptr;
+        HM_CUDA_TRY(cudaMallocHost(&h->pin_z, sizeof(double) * n * zw));
+        h->pin_z_n = (size_t)n * zw;
+    }
     HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
     for (int c0 = 0; c0 < k; c0 += zw) {
         const int kc = std::min(zw, k - c0);
@@ -276,7 +296,9 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
             src = Z + (int64_t)c0 * n;
         } else {
             h->zio.alloc(sizeof(double) * n * zw);
-            HM_CUDA_TRY(cudaMemcpyAsync(h->zio.p, Z + (int64_t)c0 * n, sizeof(double) * n * kc, cudaMemcpyHostToDevice,
+            if (c0 > 0) HM_CUDA_TRY(cudaStreamSynchronize(h->stream));   // staging buffer reused
+            std::memcpy(h->pin_z, Z + (int64_t)c0 * n, sizeof(double) * n * kc);
+            HM_CUDA_TRY(cudaMemcpyAsync(h->zio.p, h->pin_z, sizeof(double) * n * kc, cudaMemcpyHostToDevice,
                                         h->stream));
             src = h->zio.as<double>();
         }
@@ -294,11 +316,12 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
             launch_finish(h->pool.as<double>() + h->P.logd_off, h->P.n_leaves, zt, n, kc, h->out.as<double>(),
                           h->stream);
         }
-        HM_CUDA_TRY(cudaMemcpyAsync(out_host + 3 * c0, h->out.p, sizeof(double) * 3 * kc, cudaMemcpyDeviceToHost,
+        HM_CUDA_TRY(cudaMemcpyAsync(h->pin_out + 3 * c0, h->out.p, sizeof(double) * 3 * kc, cudaMemcpyDeviceToHost,
                                     h->stream));
     }
     HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
     HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    std::memcpy(out_host, h->pin_out, sizeof(double) * 3 * k);
     h->ms[2] = elapsed(h);
 }
 
