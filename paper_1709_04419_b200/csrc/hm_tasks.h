@@ -101,7 +101,11 @@ HM_HD inline bool trunc_exact_path(int32_t m, int32_t q, int32_t kmax_tot) {
     return kmax_tot <= TR_EXACT_K && m <= TR_EXACT_MMAX && q <= TR_EXACT_MMAX;
 }
 constexpr int TR_RB = 16;         // probes per block of the randomized range finder
-constexpr int TR_NB = 3;          // blocks per pass over the stacks
+#ifndef HM_TR_NB
+#define HM_TR_NB 4
+#endif
+constexpr int TR_NB = HM_TR_NB;   // blocks per pass over the stacks: 4 x 16 = 64 probes fill the
+                                  // 64-wide GEMM tiles exactly and resolve ranks up to ~48 in one pass
 constexpr int TR_PW = TR_RB * TR_NB;
 constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
 constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
