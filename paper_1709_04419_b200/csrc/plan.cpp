@@ -1096,6 +1096,9 @@ void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max) {
             P.aca.push_back(AcaTask{s.u_off, s.v_off, (int32_t)ct.lo, (int32_t)cs.lo, s.m, s.p, s.cap, s.rslot});
         }
     }
+    // largest ACA blocks first: one CTA per block, so the long ones must not start last
+    std::stable_sort(P.aca.begin(), P.aca.end(),
+                     [](const AcaTask& a, const AcaTask& b) { return (int64_t)a.m + a.q > (int64_t)b.m + b.q; });
     bld.pend.assign(nb, Pend());
     // recompression of every ACA block: a truncation with the block itself as the only piece
     bld.begin_phase(P.recompress);

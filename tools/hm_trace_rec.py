@@ -6,10 +6,10 @@ import paper_1709_04419_b200 as hm
 from synthetic import perturbed_mesh, standard_normal
 from trace_analyze import analyse
 pts, leaf, theta, eps = perturbed_mesh(256, 0.4, 2), 64, (1.0, 0.1, 0.5), 1e-7
-H = hm.HMatrix(pts, theta, eps=eps, leaf=leaf, eta=2.0, kmax=160)
+H = hm.HMatrix(pts, theta, eps=eps, leaf=leaf, eta=2.0, kmax=64)
 H.cholesky()
 T = hm.Tree(pts, leaf, 2.0)
-T.plan_dump("/tmp/plan_64k.bin", 160)
+T.plan_dump("/tmp/plan_64k.bin", 64)
 H.trace(True)
 H.assemble(theta)
 H.trace(False, "/tmp/trace_rec.bin")
