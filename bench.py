@@ -61,6 +61,14 @@ def make_points(w, seed=2):
     return uniform_iid(w["n"], seed)
 
 
+def workload_str(w, args):
+    """The configuration both arms name in their JSON line (config.workload)."""
+    if w["cfg"] == "configs[3]":
+        return f"{w['cfg']}: MC-MLE, n={w['n']}, {w['evals']} Nelder-Mead evals per replicate, eps={w['eps']}"
+    return (f"{w['cfg']}: n={w['n']} {w['kind']}, theta={w['thetas']} (ell swept +-2%), leaf={w['leaf']}, "
+            f"eta={w['eta']}, eps={w['eps']}, kmax={args.kmax}")
+
+
 def theta_schedule(w, steps):
     """Per-step theta: alternate the workload's nu values, sweep ell by +-2 %
     (a Nelder-Mead-like walk around the truth; every step is a new theta)."""
@@ -180,7 +188,7 @@ def run_reference(args, w):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{w['cfg']} n={w['n']}", "oracle_sample_n": n_s},
+            "config": {"workload": workload_str(w, args), "oracle_sample_n": n_s},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
                              "sample": f"dense Eq.(1) oracle at n={n_s} ({dt:.2f} s/eval), scaled by (n_s/n)^3"},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -258,8 +266,8 @@ def run_mc(args, w):
                 "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{w['cfg']}: {w['evals']} Nelder-Mead evals per replicate, {S} replicate(s) per "
-                                       f"rank per step (incl. their H-build and sampler), n={w['n']}, eps={w['eps']}",
+                "config": {"workload": workload_str(w, args),
+                           "step": f"{S} replicate(s) per rank (incl. their H-build and sampler)",
                            "parallelism": f"replicas x{ws}; {S} co-scheduled replicates per GPU"},
                 "estimates_rank0": res.tolist(), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
@@ -376,8 +384,7 @@ def run_gpu(args, w):
         line = {"metric": f"H-log-likelihood evals/sec at n={n}", "value": value, "unit": "evals/s",
                 "n_gpus": ws, "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{w['cfg']}: n={n} {w['kind']}, theta={w['thetas']} (ell swept +-2%),"
-                                       f" leaf={w['leaf']}, eta={w['eta']}, eps={w['eps']}, kmax={args.kmax}",
+                "config": {"workload": workload_str(w, args),
                            "l2": "no flush: H-matrix storage > 126 MB L2",
                            "parallelism": f"replicas x{ws}; {S} co-scheduled theta streams per GPU "
                                           f"(executor CTAs {caps if S > 1 else sms}, coop_max {coop}); "
