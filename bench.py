@@ -169,7 +169,7 @@ def run_reference(args, w):
     from synthetic import standard_normal, uniform_iid
     # bounded sample: dense Eq. (1) at n_s points of the workload's distribution,
     # scaled to the workload's n by the dense O(n^3) cost (the oracle is dense).
-    n_s = int(os.environ.get("HM_REF_SAMPLE_N", "3000"))
+    n_s = min(int(os.environ.get("HM_REF_SAMPLE_N", "3000")), w["n"])
     pts = make_points(w)
     rng = np.random.default_rng(5)
     sub = pts[np.sort(rng.choice(w["n"], size=n_s, replace=False))]
@@ -204,7 +204,7 @@ def cpu_baseline(w, budget_s=20.0):
     from oracle import dense as od
     from synthetic import standard_normal
     pts = make_points(w)
-    n_s = int(os.environ.get("HM_REF_SAMPLE_N", "3000"))
+    n_s = min(int(os.environ.get("HM_REF_SAMPLE_N", "3000")), w["n"])
     rng = np.random.default_rng(5)
     sub = pts[np.sort(rng.choice(w["n"], size=n_s, replace=False))]
     Z = standard_normal(n_s, 1, 7)[:, 0]
