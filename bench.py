@@ -296,7 +296,9 @@ def run_gpu(args, w):
     S = max(1, args.theta_streams)
     sms = torch.cuda.get_device_properties(lr).multi_processor_count
     caps = [sms // S + (1 if i < sms % S else 0) for i in range(S)] if S > 1 else [0]
-    coop = 8 if S > 1 else 16
+    # cooperative groups <= 8 CTAs when co-scheduled, and within the deadlock bound
+    # 4 * (coop - 1) < executor CTAs (hm_set_exec_grid)
+    coop = 16 if S == 1 else max(1, min(8, (min(caps) - 1) // 4 + 1))
     pts = make_points(w)
     n = pts.shape[0]
     steps, warm = args.steps, args.warmup
