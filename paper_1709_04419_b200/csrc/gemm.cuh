@@ -25,6 +25,11 @@ constexpr int GM_NS = 4;      // stages of the tile-VM products (staged in two 6
 #ifndef HM_GM_NSC
 #define HM_GM_NSC 4
 #endif
+#ifndef HM_GM_BKC
+#define HM_GM_BKC 16
+#endif
+constexpr int GM_BKC = HM_GM_BKC;   // K chunk of cta_gemm (truncations); 32 measured no faster
+                                    // at n = 64k (the truncations are latency-bound)
 constexpr int GM_NSC = HM_GM_NSC;   // stages of cta_gemm (truncations); 8 measured slower at
                                     // n = 64k (the truncation products are short: the ramp counts)
 
@@ -37,7 +42,7 @@ __device__ __forceinline__ GOp gop(const double* p, int64_t ld, bool trans) { re
 
 template <int BM, int BN>
 constexpr int gemm_smem_doubles() {
-    return GM_NSC * (GM_BK * (BM + 1) + GM_BK * (BN + 1));
+    return GM_NSC * (GM_BKC * (BM + 1) + GM_BKC * (BN + 1));
 }
 
 __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, bool valid) {
@@ -55,8 +60,8 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
     static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
     constexpr int FM = WM / 8, FN = WN / 8;              // DMMA blocks per warp
     constexpr int LA = BM + 1, LB = BN + 1;              // padded leading dims of the staged chunks
-    constexpr int SA = GM_BK * LA, SB = GM_BK * LB;      // doubles per stage
-    constexpr int NA = (GM_BK * BM + 255) / 256, NB = (GM_BK * BN + 255) / 256;
+    constexpr int SA = GM_BKC * LA, SB = GM_BKC * LB;      // doubles per stage
+    constexpr int NA = (GM_BKC * BM + 255) / 256, NB = (GM_BKC * BN + 255) / 256;
     double* As = smem;                                   // [stage][k][i]
     double* Bs = smem + GM_NSC * SA;                      // [stage][k][j]
     const bool tA = A.trans, tB = B.trans;
@@ -64,19 +69,19 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
     const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
-    const int nk = (Kd + GM_BK - 1) / GM_BK;
+    const int nk = (Kd + GM_BKC - 1) / GM_BKC;
     for (int tile = first; tile < tm * tn; tile += step) {
         const int i0 = (tile % tm) * BM, j0 = (tile / tm) * BN;
         auto issue = [&](int kc) {                       // chunk kc -> stage kc % NS
-            const int k0 = kc * GM_BK;
+            const int k0 = kc * GM_BKC;
             double* as = As + (kc % GM_NSC) * SA;
             double* bs = Bs + (kc % GM_NSC) * SB;
 #pragma unroll
             for (int e = 0; e < NA; ++e) {
                 const int idx = threadIdx.x + e * 256;
-                if (idx < GM_BK * BM) {
+                if (idx < GM_BKC * BM) {
                     int i, k;
-                    if (tA) { k = idx % GM_BK; i = idx / GM_BK; } else { i = idx % BM; k = idx / BM; }
+                    if (tA) { k = idx % GM_BKC; i = idx / GM_BKC; } else { i = idx % BM; k = idx / BM; }
                     const int gi = i0 + i, gk = k0 + k;
                     const bool ok = gi < M && gk < Kd;
                     cp_async8(as + k * LA + i, ok ? (tA ? A.p + gk + (int64_t)gi * A.ld : A.p + gi + (int64_t)gk * A.ld) : A.p,
@@ -86,9 +91,9 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
 #pragma unroll
             for (int e = 0; e < NB; ++e) {
                 const int idx = threadIdx.x + e * 256;
-                if (idx < GM_BK * BN) {
+                if (idx < GM_BKC * BN) {
                     int j, k;
-                    if (tB) { j = idx % BN; k = idx / BN; } else { k = idx % GM_BK; j = idx / GM_BK; }
+                    if (tB) { j = idx % BN; k = idx / BN; } else { k = idx % GM_BKC; j = idx / GM_BKC; }
                     const int gj = j0 + j, gk = k0 + k;
                     const bool ok = gj < N && gk < Kd;
                     cp_async8(bs + k * LB + j, ok ? (tB ? B.p + gj + (int64_t)gk * B.ld : B.p + gk + (int64_t)gj * B.ld) : B.p,
@@ -115,7 +120,7 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
             const double* as = As + (kc % GM_NSC) * SA;
             const double* bs = Bs + (kc % GM_NSC) * SB;
 #pragma unroll
-            for (int kk = 0; kk < GM_BK; kk += 4) {
+            for (int kk = 0; kk < GM_BKC; kk += 4) {
                 double af[FM], bf[FN];
 #pragma unroll
                 for (int a = 0; a < FM; ++a) af[a] = as[(kk + t) * LA + wm + a * 8 + g];
