@@ -14,6 +14,7 @@
 #include "common.h"
 #include "dense.h"
 #include "plan.h"
+#include "sched.h"
 #include "tree.h"
 
 struct hm_tree_s {
@@ -162,6 +163,12 @@ int hm_plan_dump(hm_tree t, int32_t kmax, const char* path, double summary[8]) {
         if (kmax <= 0) kmax = 160;
         Plan P;
         build_plan(t->T, kmax, P);
+        // the executor's ready-queue schedule of every phase, with its host replay
+        // self-check (sched.cpp): validated here without a GPU
+        for (const Phase* ph : {&P.recompress, &P.chol, &P.solve, &P.lmul}) {
+            Sched sc;
+            build_sched(*ph, sc);
+        }
         if (summary) {
             summary[0] = (double)P.pool_total;
             summary[1] = P.n_slots;

@@ -129,3 +129,14 @@ def test_unsupported_mixed_depth():
     t = Tree(uniform_iid(65, 0), 32, 2.0)
     with pytest.raises(HMError):
         t.plan_summary(64)
+
+
+def test_ready_queue_schedule_replays_on_host():
+    """The persistent executor's ready-queue schedule (sched.cpp: successor lists,
+    arrival counts, priority queues, cooperative groups pushed as consecutive slots)
+    is built for every phase of the plan and its host replay must reach every task
+    exactly once with every queue sized exactly (hm_plan_dump raises otherwise) --
+    checked here without a GPU, on a plan with cooperative truncations."""
+    from paper_1709_04419_b200 import Tree
+    s = Tree(uniform_iid(4096, 3), 32, 2.0).plan_summary(64)
+    assert s["chol_trunc_tasks"] > 0
