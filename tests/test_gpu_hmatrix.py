@@ -220,3 +220,34 @@ def test_coscheduled_handles_match_single(hm):
         Hs[0].cholesky()
     for x in Hs:
         x.close()
+
+
+@pytest.mark.parametrize("eps,tol", [(1e-8, 1e-6), (1e-5, 1e-4)])
+def test_config0_relative_eps(hm, config0, eps, tol):
+    """The other reading of the block accuracy (R4): sigma_i > eps * sigma_1 of each
+    block (hm_params.rel_eps = 1) also meets the north-star bars on configs[0]."""
+    pts, theta, Z, (oll, old, oq) = config0
+    H = hm.HMatrix(pts, theta, eps=eps, leaf=32, eta=2.0, rel_eps=True)
+    H.cholesky()
+    assert abs(H.loglik(Z)[0, 0] - oll) / abs(oll) <= tol
+
+
+@pytest.mark.parametrize("kmax,coop", [(64, 1), (160, 4), (96, 32)])
+def test_plan_parameters_do_not_change_the_answer(hm, config0, kmax, coop):
+    """Rank capacity (kmax) and the cooperative-group cap (coop_max) change the plan
+    (task chunking, CTAs per truncation), not the mathematics: configs[0] stays
+    within the north-star bar at eps = 1e-8."""
+    pts, theta, Z, (oll, old, oq) = config0
+    H = hm.HMatrix(pts, theta, eps=1e-8, leaf=32, eta=2.0, kmax=kmax, coop_max=coop)
+    H.cholesky()
+    assert abs(H.loglik(Z)[0, 0] - oll) / abs(oll) <= 1e-6
+
+
+def test_plan_parameter_validation(hm):
+    pts = uniform_iid(500, 1)
+    with pytest.raises(hm.HMError) as ei:
+        hm.HMatrix(pts, (1.0, 0.1, 0.5), eps=1e-6, leaf=32, coop_max=33)
+    assert ei.value.code == -1
+    with pytest.raises(hm.HMError) as ei:
+        hm.HMatrix(pts, (1.0, 0.1, 0.5), eps=1e-6, leaf=32, kmax=300)
+    assert ei.value.code == -1
