@@ -336,7 +336,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (!locs || !out) throw ApiError(HM_ERR_ARG, "null pointer");
         if (n < 1) throw ApiError(HM_ERR_ARG, "n >= 1 required");
         if (!(params.eps > 0.0 && params.eps < 1.0)) throw ApiError(HM_ERR_ARG, "0 < eps < 1 required");
-        if (params.leaf < 1 || params.leaf > 64) throw ApiError(HM_ERR_ARG, "1 <= leaf <= 64 required");
+        if (params.leaf < 1 || params.leaf > 128) throw ApiError(HM_ERR_ARG, "1 <= leaf <= 128 required");
         if (!(params.eta > 0.0)) throw ApiError(HM_ERR_ARG, "eta > 0 required");
         if (params.kmax <= 0) params.kmax = 160;
         if (params.coop_max <= 0) params.coop_max = TR_COOP_DEFAULT;

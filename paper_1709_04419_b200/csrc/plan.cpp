@@ -964,25 +964,24 @@ std::string Plan::summary() const {
     return buf;
 }
 
-void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max) {
-    if (T.leaf > 64) throw std::invalid_argument("leaf size > 64 is not supported by the tile VM");
+void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
+    // mixed-depth leaves (n / 2^l straddling n_min) and leaves above one 64 x 64 tile
+    // (n_min up to 128) are planned on the refined storage tree (tree.h refine_for_plan):
+    // same C~, dense blocks split into equal-depth tile-sized sub-blocks
+    Tree Tr;
+    const bool ready = plan_ready(T0, TILE_MAX_LEAF);
+    if (!ready) refine_for_plan(T0, TILE_MAX_LEAF, Tr);
+    const Tree& T = ready ? T0 : Tr;
     P = Plan();
     P.kmax = kmax;
     const int32_t nc = (int32_t)T.clusters.size();
     // leaves in tree order and per-cluster leaf ranges
     P.leaf_begin.assign(nc, 0);
     P.leaf_count.assign(nc, 0);
-    int32_t leaf_depth = -1;
     {
-        std::vector<int32_t> order;   // pre-order == storage order; leaves appear in index order
+        // pre-order == storage order; leaves appear in index order, all at one depth (plan_ready)
         for (int32_t c = 0; c < nc; ++c)
-            if (T.clusters[c].leaf()) {
-                P.leaf_cluster.push_back(c);
-                if (leaf_depth < 0) leaf_depth = T.clusters[c].level;
-                else if (leaf_depth != T.clusters[c].level)
-                    throw std::invalid_argument(
-                        "unsupported geometry: leaf clusters at different depths (n / 2^l straddles the leaf size)");
-            }
+            if (T.clusters[c].leaf()) P.leaf_cluster.push_back(c);
         P.n_leaves = (int32_t)P.leaf_cluster.size();
         // leaf_begin via post-order accumulation (children after parents in pre-order: iterate backwards)
         std::vector<int32_t> first(nc, INT32_MAX);

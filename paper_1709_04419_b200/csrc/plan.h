@@ -90,8 +90,12 @@ struct Plan {
     std::string summary() const;
 };
 
-// Build the full plan for a tree.  Throws std::invalid_argument for
-// unsupported geometry (leaf > 64, leaves at different depths).
+// Largest dense leaf block the tile VM handles in one 64 x 64 tile; trees with larger
+// leaves or leaves at several depths are planned on refine_for_plan's storage tree.
+constexpr int32_t TILE_MAX_LEAF = 64;
+
+// Build the full plan for a tree (any n >= 1, any leaf size the storage refinement can
+// halve down to TILE_MAX_LEAF without empty clusters).
 void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max = TR_COOP_DEFAULT);
 
 }  // namespace hm

@@ -51,4 +51,20 @@ void build_tree(const double* locs, int64_t n, int32_t leaf, double eta, Tree& T
 
 bool admissible(const Cluster& t, const Cluster& s, double eta);
 
+// Storage tree for the planner.  The tile VM works on dense blocks of at most
+// `maxleaf` rows and the Cholesky recursion pairs equal-depth leaves, while
+// the paper's tree (Def. 1 with n_min, reading R1) may hold leaves at two
+// depths (n / 2^l straddling n_min) and leaves above maxleaf (n_min up to 128,
+// Table 1 l.213).  R refines every leaf of T by halving its index range
+// (no reordering: tree order and perm are unchanged) until all leaves sit at
+// one depth with at most maxleaf points, and splits every dense block of T's
+// partition accordingly into dense sub-blocks.  Admissible (low-rank) blocks,
+// their clusters and T's partition of I x I are untouched, so C~ is the same
+// matrix; only the granularity of its dense part changes.  R.full_blocks is
+// empty (the partition is T's).  Throws std::invalid_argument if a leaf would
+// have to be split below one point.
+void refine_for_plan(const Tree& T, int32_t maxleaf, Tree& R);
+// true when T already has all leaves at one depth with at most maxleaf points
+bool plan_ready(const Tree& T, int32_t maxleaf);
+
 }  // namespace hm

@@ -123,12 +123,37 @@ def test_plan_summary_counts():
     assert s["chol_waves"] > 0 and s["chol_vm_tasks"] > 0 and s["solve_tasks"] > 0
 
 
-def test_unsupported_mixed_depth():
-    from paper_1709_04419_b200 import Tree, HMError
-    # 99 points, leaf 32: sizes 49/50 -> 24/25 ... leaves at one depth; 65 points, leaf 32: 32 | 33 -> mixed
-    t = Tree(uniform_iid(65, 0), 32, 2.0)
-    with pytest.raises(HMError):
-        t.plan_summary(64)
+@pytest.mark.parametrize("n,leaf,eps,seed", [(65, 32, 1e-10, 20), (1040, 32, 1e-10, 21), (1500, 100, 1e-10, 22),
+                                             (2000, 128, 1e-9, 23), (777, 48, 1e-10, 24)])
+def test_mixed_depth_and_large_leaves(tmp_path, n, leaf, eps, seed):
+    """General n (PAPER.md Def. 1 l.152-160 and n_min l.211 put no restriction on n;
+    Table 1 l.213 allows n_min up to 128): when n / 2^l straddles n_min the tree has
+    leaves at two depths (65 points, leaf 32: 32 | 33 -> 16/17), and leaves above 64
+    exceed one tile.  The planner runs on the refined storage tree (tree.h
+    refine_for_plan) -- the DAG replayed in random wave order must still match the
+    dense oracle, while the exported tree and partition stay the oracle's (bit-exact,
+    test_abi_host.py)."""
+    from paper_1709_04419_b200 import Tree
+    from oracle import geometry as og
+    pts = uniform_iid(n, seed)
+    t = Tree(pts, leaf, 2.0)
+    levels = {int(c[2]) for c in t.clusters() if c[3]}
+    big = max(int(c[1] - c[0]) for c in t.clusters() if c[3])
+    assert len(levels) > 1 or big > 64, "case must exercise the storage refinement"
+    ll, ld, q, oll, old, oq, _, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), leaf, 2.0, eps, seed=seed)
+    np.testing.assert_allclose(ll, oll, rtol=1e-8)
+    assert abs(ld - old) <= 1e-6 * abs(old) + 1e-6
+
+
+def test_paper_table2_size_plans():
+    """PAPER.md Table 2 (l.228-249): n = 16,641 on the perturbed mesh (Eq. 3) at
+    n_min = 32 (l.211), and configs[2]'s size + 1 at leaf 64: both plan (they
+    were rejected before the storage refinement)."""
+    from paper_1709_04419_b200 import Tree
+    s = Tree(perturbed_mesh(129, 0.4, seed=5), 32, 2.0).plan_summary(64)
+    assert s["chol_vm_tasks"] > 0 and s["solve_tasks"] > 0
+    s = Tree(uniform_iid(65537, 6), 64, 2.0).plan_summary(64)
+    assert s["chol_vm_tasks"] > 0
 
 
 def test_ready_queue_schedule_replays_on_host():
