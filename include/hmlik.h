@@ -10,8 +10,9 @@
  *
  * with C(theta) held in H-matrix format (sec. 2.1, Definition 1, l.152-160): a
  * geometric cluster tree over the n locations, a block cluster tree split by
- * the admissibility condition, admissible blocks compressed to relative
- * accuracy eps by ACA (l.147) + QR/SVD recompression (sec. 1 item 6, l.87),
+ * the admissibility condition, admissible blocks compressed to accuracy eps
+ * (absolute, eps * sigma^2 per block in the spectral norm: Remark 2, l.166;
+ * DESIGN.md reading R4) by ACA (l.147) + QR/SVD recompression (l.87),
  * an H-Cholesky factorisation with truncated low-rank updates (l.281-283),
  * log det = 2 sum log diag(L~) (l.283) and a forward solve for the quadratic
  * form (l.265).  DESIGN.md lists every reading of the paper this library takes.
@@ -51,7 +52,7 @@ extern "C" {
 #define HM_ERR_RANK_CAP    -4   /* a truncation needed more rank than the block capacity  */
 #define HM_ERR_OOM         -5   /* device or host allocation failed                        */
 #define HM_ERR_STATE       -6   /* call order violated (e.g. loglik before cholesky)       */
-#define HM_ERR_TOO_LARGE   -7   /* n above the dense check-path cap                        */
+#define HM_ERR_TOO_LARGE   -7   /* n above the dense check-path cap HM_DENSE_NMAX          */
 
 /* theta = (sigma^2, ell, nu), all > 0 (Eq. 2; sec. 2.2 l.187).                  */
 typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
@@ -63,7 +64,11 @@ typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
  * leaf: n_min (l.211); eta: admissibility parameter (reading R2); kmax: rank
  * capacity of one low-rank block, at most 240 (HM_ERR_RANK_CAP when exceeded;
  * 0 = default 160); coop_max: most CTAs cooperating on one truncation (1..32,
- * 0 = default 16; 8 when several handles share the GPU, see hm_set_exec_grid).  */
+ * 0 = default 16; 8 when several handles share the GPU, see hm_set_exec_grid);
+ * eps_chol: accuracy of every truncation inside the H-Cholesky (same meaning
+ * as eps; 0 = eps).  The paper fixes the accuracies of C~ and L~ separately
+ * (l.474-476, Fig. 7: 1e-3 for C~, 1e-8 for L~); Table 3 (l.483) uses one for
+ * both, which is the default.                                                 */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
@@ -71,6 +76,7 @@ typedef struct hm_params {
     int32_t kmax;
     int32_t rel_eps;
     int32_t coop_max;
+    double  eps_chol;
 } hm_params;
 
 typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */
@@ -122,8 +128,10 @@ int hm_free(hm_handle h);
  * same plan).                                                                */
 int hm_assemble(hm_handle h, hm_theta theta);
 
-/* H-Cholesky C~ = L~ L~^T in place with truncated low-rank updates (relative
- * accuracy params.eps).  HM_ERR_NOT_SPD if a pivot is not positive.          */
+/* H-Cholesky C~ = L~ L~^T in place with truncated low-rank updates (every
+ * truncation at the block accuracy of hm_params: eps * sigma^2 absolute, or
+ * eps relative with rel_eps = 1).  HM_ERR_NOT_SPD if a pivot is not positive;
+ * HM_ERR_RANK_CAP if a truncation needs more than the block's capacity.     */
 int hm_cholesky(hm_handle h);
 
 /* Log-likelihood Eq. (4) for k data vectors Z (n x k column-major, original
@@ -203,10 +211,13 @@ int hm_checksum(hm_handle h, double out[4]);
  * kernels themselves from their actual dimensions.       */
 int hm_kernel_stats(hm_handle h, double out[24]);
 
-/* ---- dense fp64 check path (n <= 16384) --------------------------------- */
+/* ---- dense fp64 check path (n <= HM_DENSE_NMAX) -------------------------- */
 /* Exact Eq. (1) on the GPU with dense Matern assembly, dense blocked
  * Cholesky, log det and forward solve; out[3*j+0..2] as in hm_loglik.
- * HM_ERR_TOO_LARGE for n > 16384.                                          */
+ * Needs 8 n^2 bytes of device memory (34 GB at n = 65,536: the configs[2]
+ * reference).  HM_ERR_TOO_LARGE for n > HM_DENSE_NMAX, HM_ERR_OOM if the
+ * matrix does not fit.                                                     */
+#define HM_DENSE_NMAX 131072
 int hm_dense_loglik(const double* locs, int32_t locs_on_device, int64_t n, hm_theta theta,
                     const double* Z, int32_t z_on_device, int32_t k,
                     int32_t device, void* stream, double* out_host);

@@ -31,7 +31,7 @@ class Theta(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32),
-                ("rel_eps", C.c_int32), ("coop_max", C.c_int32)]
+                ("rel_eps", C.c_int32), ("coop_max", C.c_int32), ("eps_chol", C.c_double)]
 
 
 def _load():
@@ -153,7 +153,8 @@ class Tree:
 
 # ---------------------------------------------------------------- dense check path
 def dense_loglik(locs, theta, Z, device: int = 0, stream=None) -> np.ndarray:
-    """Exact Eq. (1) on the GPU (n <= 16384).  Returns k x 3 (loglik, logdet, quad)."""
+    """Exact Eq. (1) on the GPU (n <= HM_DENSE_NMAX = 131072, 8 n^2 bytes of device
+    memory).  Returns k x 3 (loglik, logdet, quad)."""
     if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
         locs = _as_f64(locs)
     if isinstance(Z, np.ndarray) or not hasattr(Z, "is_cuda"):
@@ -167,6 +168,8 @@ def dense_loglik(locs, theta, Z, device: int = 0, stream=None) -> np.ndarray:
         # torch tensors: 1-D (n,) or 2-D (k, n) contiguous == column-major n x k
         k, n = (Z.shape[0], Z.shape[1]) if Z.ndim == 2 else (1, Z.shape[0])
         zp, zd = ptr_of(Z)
+    if n != int(locs.shape[0]):
+        raise ValueError(f"Z has {n} rows, locations {int(locs.shape[0])}")
     lp, ld = ptr_of(locs)
     out = np.empty((k, 3), dtype=np.float64)
     check(lib.hm_dense_loglik(lp, ld, int(locs.shape[0]), Theta(*theta), zp, zd, int(k), int(device),
@@ -203,13 +206,15 @@ class HMatrix:
     """
 
     def __init__(self, locs, theta, eps: float = 1e-8, leaf: int = 32, eta: float = 2.0, kmax: int = 160,
-                 device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0):
+                 device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0, eps_chol: float = 0.0):
         if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
             locs = _as_f64(locs)
         lp, ld = ptr_of(locs)
         self.n = int(locs.shape[0])
+        self.device = int(device)
         self._h = C.c_void_p()
-        self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0, int(coop_max))
+        self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0, int(coop_max),
+                             float(eps_chol))
         rc = lib.hm_build(lp, ld, self.n, Theta(*theta), self.params, int(device),
                           C.c_void_p(stream) if stream else None, C.byref(self._h))
         check(rc)
@@ -220,8 +225,15 @@ class HMatrix:
     def cholesky(self):
         check(lib.hm_cholesky(self._h))
 
+    def _check_rows(self, n, Z):
+        if n != self.n:
+            raise ValueError(f"data has {n} rows, the H-matrix {self.n} (torch data is (n,) or (k, n))")
+        if hasattr(Z, "is_cuda") and Z.is_cuda and Z.device.index != self.device:
+            raise ValueError(f"data on {Z.device}, handle on cuda:{self.device}")
+
     def loglik(self, Z) -> np.ndarray:
         p, d, n, k, keep = _zarg(Z)
+        self._check_rows(n, Z)
         out = np.empty((k, 3))
         check(lib.hm_loglik(self._h, p, d, int(k), out.ctypes.data_as(C.c_void_p)))
         return out
@@ -229,6 +241,7 @@ class HMatrix:
     def loglik_batch(self, thetas, Z):
         th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(-1, 3))
         p, d, n, k, keep = _zarg(Z)
+        self._check_rows(n, Z)
         out = np.empty((th.shape[0], k, 3))
         rc = lib.hm_loglik_batch(self._h, th.ctypes.data_as(C.c_void_p), th.shape[0], p, d, int(k),
                                  out.ctypes.data_as(C.c_void_p))
@@ -236,6 +249,7 @@ class HMatrix:
 
     def sample(self, xi) -> np.ndarray:
         p, d, n, k, keep = _zarg(xi)
+        self._check_rows(n, xi)
         if d:
             raise TypeError("use a host array for xi (device variant: hm_sample with device pointers)")
         out = np.empty((n, k), order="F")

@@ -215,7 +215,7 @@ int hm_dense_loglik(const double* locs, int32_t locs_on_device, int64_t n, hm_th
     try {
         if (!locs || !Z || !out_host) throw ApiError(HM_ERR_ARG, "null pointer");
         if (n < 1 || k < 1) throw ApiError(HM_ERR_ARG, "n >= 1 and k >= 1 required");
-        if (n > 16384) throw ApiError(HM_ERR_TOO_LARGE, "dense check path is limited to n <= 16384");
+        if (n > HM_DENSE_NMAX) throw ApiError(HM_ERR_TOO_LARGE, "dense check path is limited to n <= " + std::to_string(HM_DENSE_NMAX));
         check_theta(theta);
         DeviceGuard dg(device);
         cudaStream_t st = (cudaStream_t)stream;

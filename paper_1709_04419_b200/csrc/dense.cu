@@ -1,4 +1,4 @@
-// Dense fp64 check path (n <= 16384): exact Eq. (1) on the GPU.
+// Dense fp64 check path (n <= HM_DENSE_NMAX): exact Eq. (1) on the GPU.
 //
 //   assemble C(theta) (lower triangle, Eq. 2 via matern_dev)
 //   -> blocked right-looking Cholesky C = L L^T with 64 x 64 tiles

@@ -60,7 +60,9 @@ struct hm_handle_s {
     bool tracing = false;
     bool poison = false;
     bool abs_eps = true;   // block accuracy eps absolute (x sigma^2, default) or relative (rel_eps)
-    double eps_k = 0.0;    // eps as the kernels see it: > 0 relative, < 0 absolute   // HM_POISON_RING: NaN-fill the workspace ring before every phase (tests)
+    double eps_k = 0.0;    // eps as the kernels see it: > 0 relative, < 0 absolute (assembly, recompression)
+    double eps_kc = 0.0;   // the same for the truncations of the H-Cholesky (hm_params.eps_chol)
+    double eps_run = 0.0;  // the value run_phase passes to the kernels (set per phase)
     int64_t trace_n = 0;
     // profiling: per kernel family (KF_*) launch counts (always) and, when
     // enabled, a CUDA event pair around every launch on the handle's stream
@@ -165,7 +167,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         launch_exec_rq(d.xr.as<XTask>(), (int)p.xt.size(), d.su2.as<int32_t>(), d.qbase.as<int32_t>(), d.slot_init.as<int32_t>(), d.ctl_init.as<int32_t>(),
                        h->rq_cnt.as<int>(), h->rq_slot.as<int>(), h->rq_ctl.as<int>(), d.vt.as<VTask>(),
                        d.ins.as<VIns>(), d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags,
-                       ctr, h->eps_k, h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(),
+                       ctr, h->eps_run, h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(),
                        p.n_bars, d.max_nsub, h->exec_grid_cap, h->stream);
         if (h->tracing) h->trace_n = (int64_t)p.xt.size();
         HM_CUDA_TRY(cudaGetLastError());
@@ -177,7 +179,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         if (h->tracing)
             HM_CUDA_TRY(cudaMemsetAsync((char*)h->trace.p + 32 * p.xt.size(), 0, 8 * 64 * p.xt.size(), h->stream));
         launch_exec(d.xt.as<XTask>(), (int)p.xt.size(), d.xd.as<int32_t>(), d.vt.as<VTask>(), d.ins.as<VIns>(),
-                    d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->eps_k, h->done.as<int>(),
+                    d.terms.as<VTerm>(), d.tt.as<TTask>(), d.tp.as<TPiece>(), pool, ranks, flags, ctr, h->eps_run, h->done.as<int>(),
                     h->counter.as<int>(), h->epoch,
                     h->tracing ? (unsigned long long*)h->trace.p : nullptr, h->bars.as<int>(), p.n_bars, h->stream);
         if (h->tracing) h->trace_n = (int64_t)p.xt.size();
@@ -189,7 +191,7 @@ void run_phase(hm_handle_s* h, const DPhase& d) {
         const int t0 = p.t_wave_begin[w], t1 = p.t_wave_begin[w + 1];
         if (t1 > t0) {
             Launch L(h, KF_TRUNC);
-            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->eps_k, ctr,
+            launch_trunc(d.tt.as<TTask>() + t0, t1 - t0, d.tp.as<TPiece>(), pool, ranks, flags, h->eps_run, ctr,
                          h->stream);
         }
         if (v1 > v0) {
@@ -228,6 +230,8 @@ void do_assemble(hm_handle_s* h, hm_theta th) {
     check_theta(th);
     h->theta = th;
     h->eps_k = h->abs_eps ? -h->prm.eps * th.sigma2 : h->prm.eps;
+    h->eps_kc = h->abs_eps ? -h->prm.eps_chol * th.sigma2 : h->prm.eps_chol;
+    h->eps_run = h->eps_k;
     matern_setup(th.sigma2, th.ell, th.nu, h->mp);
     HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
     HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
@@ -259,7 +263,9 @@ void do_cholesky(hm_handle_s* h) {
     if (h->factored) throw ApiError(HM_ERR_STATE, "hm_cholesky: already factored (re-assemble first)");
     HM_CUDA_TRY(cudaMemsetAsync(h->flags.p, 0, sizeof(int) * 4, h->stream));
     HM_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+    h->eps_run = h->eps_kc;
     run_phase(h, h->chol);
+    h->eps_run = h->eps_k;
     HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
     int f[4];
     read_flags(h, f);
@@ -336,6 +342,8 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (!locs || !out) throw ApiError(HM_ERR_ARG, "null pointer");
         if (n < 1) throw ApiError(HM_ERR_ARG, "n >= 1 required");
         if (!(params.eps > 0.0 && params.eps < 1.0)) throw ApiError(HM_ERR_ARG, "0 < eps < 1 required");
+        if (params.eps_chol == 0.0) params.eps_chol = params.eps;
+        if (!(params.eps_chol > 0.0 && params.eps_chol < 1.0)) throw ApiError(HM_ERR_ARG, "0 < eps_chol < 1 required");
         if (params.leaf < 1 || params.leaf > 128) throw ApiError(HM_ERR_ARG, "1 <= leaf <= 128 required");
         if (!(params.eta > 0.0)) throw ApiError(HM_ERR_ARG, "eta > 0 required");
         if (params.kmax <= 0) params.kmax = 160;

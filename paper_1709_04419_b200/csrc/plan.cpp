@@ -16,7 +16,8 @@
 //   * a dense leaf applies all its pieces/products in one tile-VM program,
 //     then POTRF (diagonal) or TRSM (off-diagonal);
 //   * a low-rank block gathers [own U V^T, pieces, evaluated products] and is
-//     re-truncated ONCE (QR + SVD, sigma_i > eps sigma_1) -- the "truncated
+//     re-truncated ONCE (QR + SVD, sigma_i > tau, tau = eps sigma^2 by default,
+//     reading R4) -- the "truncated
 //     low-rank updates" of the north star -- then its V is forward-solved.
 // Every task declares the device regions it reads/writes (row chunks at leaf
 // clusters); a task's wave is 1 + the latest wave it depends on, so each
@@ -28,6 +29,7 @@
 #include <climits>
 #include <cstring>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <utility>
 
@@ -1126,6 +1128,10 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
     for (Phase* ph : {&P.recompress, &P.chol, &P.solve, &P.lmul})
         for (TTask& t : ph->tt) t.ws += P.ring_off;
     P.pool_total = bld.bump;
+    if (std::getenv("HM_PLAN_VERBOSE"))
+        std::fprintf(stderr, "plan: blocks(C~ at capacity)=%.3f GB z=%.3f GB tmp=%.3f GB ring=%.3f GB other temporaries=%.3f GB total=%.3f GB\n",
+                     8e-9 * P.bytes_C / 8, 8e-9 * (double)T.n * P.zw, 8e-9 * 8192 * 4096.0, 8e-9 * P.ring_size,
+                     8e-9 * (P.pool_total - P.pool_blocks - 8192 * 4096.0 - P.ring_size), 8e-9 * P.pool_total);
 }
 
 }  // namespace hm

@@ -1,7 +1,7 @@
 // Low-rank truncation kernel k_trunc ("efficient rank-truncation
 // techniques"; adaptive-rank strategy of Remark 2, l.166, reading R4):
 //
-//   B <- best rank-r approximation, sigma_i > eps * sigma_1, of
+//   B <- best rank-r approximation, sigma_i > tau, of
 //        M = sum_p alpha_p pad(U_p) pad(V_p)^T        (m x q, K = sum_p width_p)
 //
 // Two algorithms, chosen per task by the planner's static width bound:
@@ -13,9 +13,9 @@
 //    finder on the implicit sum (Halko, Martinsson & Tropp, Alg. 4.2 with the
 //    a-posteriori bound of their Lemma 4.1): rounds of RB Gaussian probes
 //    Y = M Omega computed piece by piece (never forming M or the stacks),
-//    twice-projected against the basis Q, stop when every projected probe has
-//    norm <= eps * sigma_est / 8 (so ||M - Q Q^T M|| <= eps sigma_1 with
-//    probability >= 1 - 10^-RB); then W = M^T Q (again piece by piece),
+//    twice-projected against the basis Q, stop when every projected probe of a
+//    round has norm <= TR_STOP * tau (an estimate of ||M - Q Q^T M||_F, which
+//    bounds the spectral error); then W = M^T Q (again piece by piece),
 //    Householder QR W = Q_W R, Jacobi SVD of R^T, U = Q X Sigma, V = Q_W Z.
 //    Work is linear in K (about 4 (m + q) K (ell + RB) flops), and the only
 //    dense SVD is ell x ell with ell = rank + RB.
@@ -41,23 +41,20 @@ namespace hm {
 
 constexpr int TR_THREADS = 256;
 
-// truncation threshold: eps > 0 relative (sigma_i > eps sigma_1), eps < 0 absolute
-// (sigma_i > |eps|; hm_params.abs_eps, the paper's Remark 2 wording)
+// truncation threshold tau: eps > 0 relative (sigma_i > eps sigma_1), eps < 0 absolute
+// (sigma_i > |eps| = eps * sigma^2, the default: the paper's Remark 2 wording, reading R4)
 __device__ __forceinline__ double tr_cut(double eps, double smax) { return eps > 0.0 ? eps * smax : -eps; }
 constexpr int ORDER_MAX = 512;
 // Range-finder stopping rule.  For a Gaussian probe w, E ||R w||^2 = ||R||_F^2, so
 // the probe norms ||M w_j|| estimate ||M||_F and the projected-probe norms
 // ||(I - Q Q^T) M w_j|| estimate ||M - Q Q^T M||_F.  The basis is complete when
-// every projected probe of a round is <= TR_STOP * eps * max_j ||M w_j||:
-// relative accuracy ~TR_STOP * eps in the Frobenius norm (hence also in the
-// spectral one) before the final SVD truncation at eps * sigma_1.  TR_STOP = 4
-// lets the residual keep the noise floor of the accumulated updates (measured:
-// parity tests unchanged, basis widths ~40 % smaller than with TR_STOP = 1).  (A spectral
-// certificate would have to capture the flat tail of truncation noise the
-// accumulated Cholesky updates carry just below eps * sigma_1: ~4x the final
-// rank measured at n = 64k.)
+// every projected probe of a round is <= TR_STOP * tau (tau = the truncation threshold,
+// |eps| absolute or eps * max_j ||M w_j|| relative): Frobenius accuracy ~TR_STOP * tau,
+// hence also spectral, before the final SVD truncation at tau.  TR_STOP = 1 certifies
+// Remark 2's "accuracy eps or better" per block (l.166-167); the round-1 value 4 kept
+// the noise floor of the accumulated updates (bases ~40 % narrower) at ~4 tau.
 #ifndef HM_TR_STOP
-#define HM_TR_STOP 4.0
+#define HM_TR_STOP 1.0
 #endif
 constexpr double TR_STOP = HM_TR_STOP;
 // eps from which the final SVD of the projected block uses the Gram matrix (see F3)
