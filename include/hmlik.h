@@ -202,6 +202,17 @@ int hm_trace(hm_handle h, int32_t enable, const char* path);
  * of the ranks.  Copies the block storage to the host (slow; tests only).     */
 int hm_checksum(hm_handle h, double out[4]);
 
+/* Diagnostics: the matrix the handle currently holds -- C~ after hm_build /
+ * hm_assemble (symmetric: its stored lower block triangle mirrored), L~ after
+ * hm_cholesky (lower triangular in tree order) -- expanded to a dense n x n
+ * column-major host array in the ORIGINAL point order, out[pi + pj*n] with
+ * (pi, pj) = (perm[i], perm[j]) for tree positions (i, j), so that the C~ of
+ * the output approximates C(theta) entry by entry and out * out^T (for L~)
+ * approximates it as a whole.  8 n^2 bytes, expanded on the host (tests and
+ * diagnostics only).  HM_ERR_STATE before any assembly, HM_ERR_TOO_LARGE for
+ * n > HM_DENSE_NMAX.                                                         */
+int hm_to_dense(hm_handle h, double* out_host);
+
 /* Per kernel family f = 0..5 (dense Matern block generation, ACA, low-rank
  * truncation, tile VM, auxiliary gather/finish, persistent executor -- whose
  * flops/bytes are those of the truncation + VM tasks it ran): out[4f + 0] launches since

@@ -65,6 +65,7 @@ def _load():
         "hm_set_exec_grid": ([P, I32], C.c_int),
         "hm_trace": ([P, I32, C.c_char_p], C.c_int),
         "hm_checksum": ([P, P], C.c_int),
+        "hm_to_dense": ([P, P], C.c_int),
         "hm_dense_loglik": ([P, I32, I64, Theta, P, I32, I32, I32, P, P], C.c_int),
         "hm_matern_block": ([P, I64, P, I64, Theta, I32, P], C.c_int),
     }
@@ -79,7 +80,7 @@ lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
             "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_stats", "hm_timings", "hm_profile",
-            "hm_kernel_stats", "hm_set_exec_mode", "hm_set_exec_grid", "hm_trace", "hm_checksum",
+            "hm_kernel_stats", "hm_set_exec_mode", "hm_set_exec_grid", "hm_trace", "hm_checksum", "hm_to_dense",
             "hm_dense_loglik", "hm_matern_block")
 
 
@@ -291,6 +292,13 @@ class HMatrix:
         s = np.zeros(4)
         check(lib.hm_checksum(self._h, s.ctypes.data_as(C.c_void_p)))
         return s
+
+    def to_dense(self) -> np.ndarray:
+        """C~ (after assembly) or L~ (after cholesky) as a dense n x n array in the
+        original point order (diagnostics; hm_to_dense)."""
+        out = np.empty((self.n, self.n), order="F")
+        check(lib.hm_to_dense(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def kernel_stats(self) -> dict:
         s = np.zeros(24)

@@ -625,6 +625,50 @@ int hm_checksum(hm_handle h, double out[4]) {
     }
 }
 
+int hm_to_dense(hm_handle h, double* out) {
+    try {
+        if (!h || !out) throw ApiError(HM_ERR_ARG, "null pointer");
+        const int64_t n = h->T.n;
+        if (n > HM_DENSE_NMAX) throw ApiError(HM_ERR_TOO_LARGE, "hm_to_dense: n above HM_DENSE_NMAX");
+        if (!h->assembled && !h->factored) throw ApiError(HM_ERR_STATE, "hm_to_dense: nothing assembled");
+        DeviceGuard dg(h->device);
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        const Plan& P = h->P;
+        std::vector<double> pool((size_t)P.pool_blocks);
+        HM_CUDA_TRY(cudaMemcpy(pool.data(), h->pool.p, sizeof(double) * pool.size(), cudaMemcpyDeviceToHost));
+        max_rank(h);
+        const bool lower = h->factored;   // L~: lower triangular; C~: symmetric
+        std::vector<double> M((size_t)(n * n), 0.0);   // tree order, column-major
+        auto put = [&](int64_t i, int64_t j, double v) {
+            if (i == j || i > j) M[(size_t)(i + j * n)] = v;
+            if (!lower && i != j) M[(size_t)(j + i * n)] = v;
+        };
+        for (const DenseGenTask& d : P.dgen)
+            for (int64_t j = 0; j < d.q; ++j)
+                for (int64_t i = 0; i < d.m; ++i) {
+                    const int64_t gi = d.r0 + i, gj = d.c0 + j;
+                    if (gi < gj) continue;   // diagonal blocks: upper part is mirrored / zero
+                    put(gi, gj, pool[(size_t)(d.off + i + j * d.m)]);
+                }
+        for (const AcaTask& a : P.aca) {
+            const int r = h->h_ranks[a.rslot];
+            for (int64_t j = 0; j < a.q; ++j)
+                for (int64_t i = 0; i < a.m; ++i) {
+                    double v = 0.0;
+                    for (int k = 0; k < r; ++k)
+                        v += pool[(size_t)(a.u_off + i + (int64_t)k * a.m)] * pool[(size_t)(a.v_off + j + (int64_t)k * a.q)];
+                    put(a.r0 + i, a.c0 + j, v);
+                }
+        }
+        const int64_t* pm = h->T.perm.data();
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) out[pm[i] + pm[j] * n] = M[(size_t)(i + j * n)];
+        return HM_OK;
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
 int hm_trace(hm_handle h, int32_t enable, const char* path) {
     try {
         if (!h) throw ApiError(HM_ERR_ARG, "null handle");

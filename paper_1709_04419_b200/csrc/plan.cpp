@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <map>
+#include <set>
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
@@ -80,6 +82,21 @@ struct Builder {
     // every chunk is a resource, so reuse of a region orders after its last user
     int64_t ring_chunk = 0, ring_nchunks = 0, ring_ptr = 0;
     std::vector<int32_t> ring_res;                  // resource id of each chunk (the ring can grow)
+    // temporary arena for the H x thin products (Thin::tmp) and their cores: an allocation
+    // lives until the last pending piece referring to it is consumed (reference count);
+    // its extent then returns to a free list together with "fence" tasks (the tasks that
+    // touched it), and the first access of every resource later placed on that memory
+    // waits for them (pre).  Offsets are arena_base + relative offset.
+    struct TmpAlloc { int64_t off, len; int32_t res0, nres, refs; };
+    std::vector<TmpAlloc> tmps;
+    struct Ext { int64_t len; std::vector<int32_t> fences; int32_t fwave; };
+    std::map<int64_t, Ext> afree;                                  // free extents by offset
+    std::vector<std::set<std::pair<int32_t, int64_t>>> aclass;     // per size class: (fence wave, off)
+    int64_t arena_base = 0, arena_top = 0;
+    int arena_mode = 1;   // experiments (HM_ARENA_MODE): 0 never recycle, 1 wave rule, 2 any free extent
+    int64_t arena_budget = INT64_MAX;   // doubles; above it, recycling ignores the wave rule
+    std::vector<std::vector<int32_t>> pre;          // per resource: tasks its first access waits for
+    static constexpr size_t FENCE_MAX = 8;
     // current phase state
     Phase* ph = nullptr;
     std::vector<std::pair<int32_t, VTask>> vraw;   // (wave, task)
@@ -103,6 +120,7 @@ struct Builder {
         rd_wave.resize(nres, -1);
         lw_task.resize(nres, -1);
         rd_tasks.resize(nres);
+        pre.resize(nres);
         return b;
     }
 
@@ -111,11 +129,162 @@ struct Builder {
         ring_nchunks = (int64_t)ring_res.size();
     }
 
+    // ---- temporary arena ----------------------------------------------------
+    // A task with no instructions that depends on `deps`: one edge per dependency
+    // instead of (new users) x (old users) edges when memory is recycled.
+    int32_t noop_task(std::vector<int32_t> deps) {
+        std::sort(deps.begin(), deps.end());
+        deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+        int32_t w = 0;
+        for (int32_t d : deps) w = std::max(w, xraw[d].wave + 1);
+        VTask t;
+        t.ins_begin = (int32_t)ph->ins.size();
+        t.ins_count = 0;
+        xraw.push_back({w, 0, (int32_t)vraw.size(), std::move(deps)});
+        vraw.push_back({w, t});
+        ++n_tasks;
+        return (int32_t)xraw.size() - 1;
+    }
+    void compress_fences(std::vector<int32_t>& f) {
+        std::sort(f.begin(), f.end());
+        f.erase(std::unique(f.begin(), f.end()), f.end());
+        if (f.size() > FENCE_MAX) f = {noop_task(f)};
+    }
+    static int size_class(int64_t len) {   // floor(log2(len / 32))
+        int c = 0;
+        for (int64_t v = len >> 5; v > 1; v >>= 1) ++c;
+        return c;
+    }
+    void ext_unlink(int64_t off, const Ext& e) { aclass[size_class(e.len)].erase({e.fwave, off}); }
+    void arena_insert(int64_t off, int64_t len, std::vector<int32_t> f) {
+        auto nx = afree.lower_bound(off);
+        if (nx != afree.end() && nx->first == off + len) {
+            len += nx->second.len;
+            f.insert(f.end(), nx->second.fences.begin(), nx->second.fences.end());
+            ext_unlink(nx->first, nx->second);
+            afree.erase(nx);
+        }
+        auto pv = afree.lower_bound(off);
+        if (pv != afree.begin()) {
+            --pv;
+            if (pv->first + pv->second.len == off) {
+                off = pv->first;
+                len += pv->second.len;
+                f.insert(f.end(), pv->second.fences.begin(), pv->second.fences.end());
+                ext_unlink(pv->first, pv->second);
+                afree.erase(pv);
+            }
+        }
+        compress_fences(f);
+        int32_t fw = -1;
+        for (int32_t t : f) fw = std::max(fw, xraw[t].wave);
+        const int c = size_class(len);
+        if ((int)aclass.size() <= c) aclass.resize(c + 1);
+        aclass[c].insert({fw, off});
+        afree[off] = Ext{len, std::move(f), fw};
+    }
+    // Allocation policy.  Recycling memory adds dependencies on the tasks that used it
+    // last (its fences); those are harmless only if they finish before the new user
+    // could start anyway.  The planner's proxy for "anyway" is the wave: reuse a free
+    // extent only if its fences sit in an earlier wave than `wnat` (the wave of the
+    // data the new allocation is computed from), oldest fences first; else grow the arena.
+    int64_t arena_take(int64_t len, int32_t wnat, std::vector<int32_t>& fences) {
+        len = (len + 31) & ~int64_t(31);   // 256-byte alignment
+        int64_t best = -1;
+        int32_t bw = INT32_MAX;
+        if (arena_mode == 0) wnat = INT32_MIN;
+        if (arena_mode == 2) wnat = INT32_MAX;
+        // over the budget: recycle the extent with the oldest fences even if they are late
+        const bool over = arena_top + len > arena_budget;
+        for (int c = size_class(len); c < (int)aclass.size(); ++c) {
+            int scanned = 0;
+            for (const auto& e : aclass[c]) {
+                if ((!over && e.first >= wnat) || e.first >= bw) break;
+                if (afree[e.second].len >= len) {
+                    best = e.second;
+                    bw = e.first;
+                    break;
+                }
+                if (++scanned > 16) break;
+            }
+        }
+        if (best >= 0) {
+            auto fit = afree.find(best);
+            Ext e = std::move(fit->second);
+            ext_unlink(best, e);
+            afree.erase(fit);
+            fences = e.fences;
+            if (e.len > len) arena_insert(best + len, e.len - len, std::move(e.fences));
+            return best;
+        }
+        fences.clear();
+        const int64_t off = arena_top;
+        arena_top += len;
+        return off;
+    }
+    // new arena allocation of n doubles whose memory is covered by resources [res0, res0 + nres)
+    double site_bytes[4] = {0, 0, 0, 0};
+    int cur_site = 0;
+    int32_t tmp_new(int64_t n, int32_t res0, int32_t nres, int32_t wnat, int64_t& off) {
+        site_bytes[cur_site] += 8.0 * n;
+        std::vector<int32_t> f;
+        const int64_t rel = arena_take(n, wnat, f);
+        for (int32_t r = res0; r < res0 + nres; ++r) pre[r] = f;
+        tmps.push_back({rel, (n + 31) & ~int64_t(31), res0, nres, 0});
+        off = arena_base + rel;
+        return (int32_t)tmps.size() - 1;
+    }
+    void tmp_release(int32_t id) {
+        const TmpAlloc a = tmps[id];
+        std::vector<int32_t> f;
+        for (int32_t r = a.res0; r < a.res0 + a.nres; ++r) {
+            if (lw_task[r] >= 0) f.push_back(lw_task[r]);
+            f.insert(f.end(), rd_tasks[r].begin(), rd_tasks[r].end());
+            f.insert(f.end(), pre[r].begin(), pre[r].end());   // never accessed: keep the old fences
+            pre[r].clear();
+        }
+        arena_insert(a.off, a.len, std::move(f));
+    }
+    void tmp_ref(const Thin& t, int d) {
+        if (t.tmp < 0) return;
+        int32_t& r = tmps[t.tmp].refs;
+        r += d;
+        if (r < 0) throw std::logic_error("planner: temporary released twice");
+        if (r == 0) tmp_release(t.tmp);
+    }
+    void piece_ref(const LPiece& pc, int d) {
+        tmp_ref(pc.U, d);
+        tmp_ref(pc.V, d);
+    }
+    // phases run one after another: fences of an earlier phase are met
+    void arena_new_phase() {
+        std::map<int64_t, Ext> old;
+        old.swap(afree);
+        aclass.clear();
+        for (auto& e : old) arena_insert(e.first, e.second.len, {});
+        for (auto& v : pre) v.clear();
+    }
+    // wave after which the data in resources `rs` (a product's source) is available
+    int32_t avail_wave(const Thin& M) const {
+        int32_t w = 0;
+        for (int32_t i = 0; i < P.leaf_count[M.cluster]; ++i) w = std::max(w, lw_wave[M.res0 + i] + 1);
+        return w;
+    }
+
     // ---- dependency tracking ------------------------------------------
     int32_t wave_of(const std::vector<int32_t>& reads, const std::vector<int32_t>& writes,
                     std::vector<int32_t>& deps) {
         const int32_t me = (int32_t)xraw.size();
         deps.clear();
+        int32_t wpre = 0;
+        // first access to memory recycled from the temporary arena: after its fences
+        for (const auto* rs : {&reads, &writes})
+            for (int32_t r : *rs)
+                for (int32_t f : pre[r]) {
+                    deps.push_back(f);
+                    wpre = std::max(wpre, xraw[f].wave + 1);
+                }
+        for (int32_t r : writes) pre[r].clear();
         for (int32_t r : reads)
             if (lw_task[r] >= 0) deps.push_back(lw_task[r]);
         for (int32_t r : writes) {
@@ -129,7 +298,7 @@ struct Builder {
             lw_task[r] = me;
             rd_tasks[r].clear();
         }
-        int32_t w = 0;
+        int32_t w = wpre;
         for (int32_t r : reads)
             if (lw_wave[r] >= 0) w = std::max(w, lw_wave[r] + 1);
         for (int32_t r : writes) {
@@ -275,14 +444,14 @@ struct Builder {
     void thin_res(const Thin& M, std::vector<int32_t>& out) const {
         for (int32_t i = 0; i < P.leaf_count[M.cluster]; ++i) out.push_back(M.res0 + i);
     }
-    Thin new_thin(int32_t cluster, int32_t cols, int32_t slot) {
+    Thin new_thin(int32_t cluster, int32_t cols, int32_t slot, int32_t wnat) {
         Thin t;
         t.cluster = cluster;
         t.ld = (int32_t)C(cluster).size();
         t.cols = cols;
         t.slot = slot;
-        t.off = alloc((int64_t)t.ld * cols);
         t.res0 = new_res(P.leaf_count[cluster]);
+        t.tmp = tmp_new((int64_t)t.ld * cols, t.res0, P.leaf_count[cluster], wnat, t.off);
         return t;
     }
     Thin thin_U(int32_t b) const {
@@ -413,7 +582,7 @@ struct Builder {
         // stage A: cores of the low-rank leaves, core_b = V_b^T Vsrc|_{s_b}
         std::vector<int32_t> stack{Y}, lr_leaves;
         const int32_t noc = (W + 63) / 64;
-        struct Core { int64_t off; int32_t res; };   // res: one resource per (kc, oc) chunk
+        struct Core { int64_t off; int32_t res; int32_t tmp; };   // res: one resource per (kc, oc) chunk
         std::vector<std::pair<int32_t, Core>> cores;
         while (!stack.empty()) {
             int32_t b = stack.back();
@@ -429,8 +598,10 @@ struct Builder {
         for (int32_t b : lr_leaves) {
             const BStore& s = P.bs[b];
             Core cr;
-            cr.off = alloc((int64_t)s.cap * W);
-            cr.res = new_res(((s.cap + 63) / 64) * noc);
+            const int32_t nr = ((s.cap + 63) / 64) * noc;
+            cr.res = new_res(nr);
+            cur_site = 3;
+            cr.tmp = tmp_new((int64_t)s.cap * W, cr.res, nr, std::max(avail_wave(thin_V(b)), avail_wave(Vsrc)), cr.off);
             const Thin Vb = thin_V(b);
             const Thin Vs = sub(Vsrc, B(b).s);
             std::vector<int32_t> lv;
@@ -513,6 +684,7 @@ struct Builder {
                 }
             }
         }
+        for (auto& pr : cores) tmp_release(pr.second.tmp);
     }
 
     // ---- forward substitution  V <- L(s,s)^{-1} V --------------------------
@@ -612,13 +784,17 @@ struct Builder {
                     for (int j = 0; j < 2; ++j)
                         pend[c[0]].prods.push_back({B(X).child[c[1] + 2 * j], B(Y).child[c[2] + 2 * j]});
             } else if (kx == ST_LR) {
-                Thin Tm = new_thin(bb.s, P.bs[X].cap, P.bs[X].rslot);
+                cur_site = 1;
+                Thin Tm = new_thin(bb.s, P.bs[X].cap, P.bs[X].rslot, avail_wave(thin_V(X)));
                 hxt(Y, thin_V(X), Tm, 1.0, false);
                 pd.pieces.push_back(LPiece{thin_U(X), Tm, -1.0});
+                piece_ref(pd.pieces.back(), +1);
             } else if (ky == ST_LR) {
-                Thin Tm = new_thin(bb.t, P.bs[Y].cap, P.bs[Y].rslot);
+                cur_site = 1;
+                Thin Tm = new_thin(bb.t, P.bs[Y].cap, P.bs[Y].rslot, avail_wave(thin_V(Y)));
                 hxt(X, thin_V(Y), Tm, 1.0, false);
                 pd.pieces.push_back(LPiece{Tm, thin_U(Y), -1.0});
+                piece_ref(pd.pieces.back(), +1);
             } else {
                 throw std::logic_error("push_down: dense factor above the leaf level");
             }
@@ -627,7 +803,9 @@ struct Builder {
             for (auto& c : ch) {
                 const Block& cb = B(c[0]);
                 pend[c[0]].pieces.push_back(LPiece{sub(pc.U, cb.t), sub(pc.V, cb.s), pc.alpha});
+                piece_ref(pend[c[0]].pieces.back(), +1);
             }
+            piece_ref(pc, -1);
         }
     }
 
@@ -637,9 +815,12 @@ struct Builder {
     // accumulates its partial sum into a temporary tile (ring of 64 x 64 slots) as
     // soon as its own operands exist; the target's task then only adds the partials.
     // This moves the bulk of the update off the Cholesky's critical path.
-    void apply_dense_pending(Prog& pg, int32_t b) {
+    // The pieces consumed are appended to `rel`: the caller drops their references after
+    // emitting the target's program (which may read them).
+    void apply_dense_pending(Prog& pg, int32_t b, std::vector<LPiece>& rel) {
         Pend pd = std::move(pend[b]);
         pend[b] = Pend();
+        rel.insert(rel.end(), pd.pieces.begin(), pd.pieces.end());
         std::vector<Prog> terms;
         for (auto& pr : pd.prods) {
             const int32_t X = pr.first, Y = pr.second;
@@ -701,16 +882,20 @@ struct Builder {
 
     // evaluate product X Y^T into truncation pieces placed at (row0, col0) of the target
     void eval_pieces(int32_t X, int32_t Y, int32_t row0, int32_t col0, std::vector<TPiece>& out,
-                     std::vector<int32_t>& reads) {
+                     std::vector<int32_t>& reads, std::vector<Thin>& temps) {
         const int32_t kx = P.bs[X].kind, ky = P.bs[Y].kind;
         if (kx == ST_LR) {
-            Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot);
+            cur_site = 2;
+            Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot, avail_wave(thin_V(X)));
             hxt(Y, thin_V(X), Tm, 1.0, false);
             out.push_back(tpiece(thin_U(X), Tm, row0, col0, -1.0, reads));
+            temps.push_back(Tm);
         } else if (ky == ST_LR) {
-            Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot);
+            cur_site = 2;
+            Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot, avail_wave(thin_V(Y)));
             hxt(X, thin_V(Y), Tm, 1.0, false);
             out.push_back(tpiece(Tm, thin_U(Y), row0, col0, -1.0, reads));
+            temps.push_back(Tm);
         } else if (kx == ST_DENSE && ky == ST_DENSE) {
             out.push_back(tpiece(thin_D(X), thin_D(Y), row0, col0, -1.0, reads));
         } else if (kx == ST_SUB && ky == ST_SUB) {
@@ -721,7 +906,7 @@ struct Builder {
                     for (int j = 0; j < 2; ++j) {
                         const int32_t cx = B(X).child[i + 2 * j], cy = B(Y).child[k + 2 * j];
                         eval_pieces(cx, cy, row0 + (int32_t)(C(B(cx).t).lo - rx.lo),
-                                    col0 + (int32_t)(C(B(cy).t).lo - ry.lo), out, reads);
+                                    col0 + (int32_t)(C(B(cy).t).lo - ry.lo), out, reads, temps);
                     }
         } else {
             throw std::logic_error("eval_pieces: mixed dense/subdivided factors");
@@ -747,12 +932,18 @@ struct Builder {
         if (!force && pd.prods.empty() && pd.pieces.empty()) return;
         std::vector<TPiece> pcs;
         std::vector<int32_t> reads, writes;
+        std::vector<Thin> temps;
         pcs.push_back(tpiece(thin_U(b), thin_V(b), 0, 0, 1.0, reads));
         for (auto& pc : pd.pieces) pcs.push_back(tpiece(pc.U, pc.V, 0, 0, pc.alpha, reads));
-        for (auto& pr : pd.prods) eval_pieces(pr.first, pr.second, 0, 0, pcs, reads);
+        for (auto& pr : pd.prods) eval_pieces(pr.first, pr.second, 0, 0, pcs, reads, temps);
         thin_res(thin_U(b), writes);
         thin_res(thin_V(b), writes);
         emit_trunc(b, pcs, reads, writes);
+        for (auto& pc : pd.pieces) piece_ref(pc, -1);
+        for (auto& t : temps) {
+            tmp_ref(t, +1);
+            tmp_ref(t, -1);
+        }
     }
 
     void emit_trunc(int32_t b, const std::vector<TPiece>& pcs, std::vector<int32_t>& reads,
@@ -825,8 +1016,9 @@ struct Builder {
             }
         } else {
             Prog pg;
+            std::vector<LPiece> rel;
             ld_dense(pg, 0, d);
-            apply_dense_pending(pg, d);
+            apply_dense_pending(pg, d, rel);
             const int32_t li = P.leaf_begin[t];
             op2(pg, VM_POTRF, 0, 0, P.logd_off + li);
             st_dense(pg, 0, d);
@@ -839,6 +1031,7 @@ struct Builder {
                 pg.writes.push_back(sd.inv_res);
             }
             emit_vm(pg);
+            for (auto& pc : rel) piece_ref(pc, -1);
         }
     }
 
@@ -854,12 +1047,14 @@ struct Builder {
             for (int i = 0; i < 2; ++i) trsm(bb.child[i + 2]);                 // (r_i, s1)
         } else if (st.kind == ST_DENSE) {
             Prog pg;
+            std::vector<LPiece> rel;
             ld_dense(pg, 0, b);
-            apply_dense_pending(pg, b);
+            apply_dense_pending(pg, b, rel);
             ld_inv(pg, 1, P.diag_of[s]);                // B <- B L^{-T} = B (L^{-1})^T
             gemm(pg, 2, 0, false, 1, true, 1.0, 0.0);
             st_dense(pg, 2, b);
             emit_vm(pg);
+            for (auto& pc : rel) piece_ref(pc, -1);
         } else {
             flush_lr(b, false);
             fsolve(s, thin_V(b));
@@ -875,6 +1070,7 @@ struct Builder {
         xraw.clear();
         ring_ptr = 0;
         tmp_ptr = 0;
+        arena_new_phase();
         std::fill(lw_wave.begin(), lw_wave.end(), -1);
         std::fill(rd_wave.begin(), rd_wave.end(), -1);
         std::fill(lw_task.begin(), lw_task.end(), -1);
@@ -966,7 +1162,7 @@ std::string Plan::summary() const {
     return buf;
 }
 
-void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
+void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t arena_budget) {
     // mixed-depth leaves (n / 2^l straddling n_min) and leaves above one 64 x 64 tile
     // (n_min up to 128) are planned on the refined storage tree (tree.h refine_for_plan):
     // same C~, dense blocks split into equal-depth tile-sized sub-blocks
@@ -1101,6 +1297,11 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
     std::stable_sort(P.aca.begin(), P.aca.end(),
                      [](const AcaTask& a, const AcaTask& b) { return (int64_t)a.m + a.q > (int64_t)b.m + b.q; });
     bld.pend.assign(nb, Pend());
+    // temporaries of every phase live in one arena above the permanent storage
+    bld.arena_base = bld.bump;
+    if (const char* am = std::getenv("HM_ARENA_MODE")) bld.arena_mode = std::atoi(am);
+    bld.arena_budget = arena_budget;
+    if (const char* ab = std::getenv("HM_ARENA_BUDGET")) bld.arena_budget = std::atoll(ab);
     // recompression of every ACA block: a truncation with the block itself as the only piece
     bld.begin_phase(P.recompress);
     for (int32_t b : lr_order) bld.flush_lr(b, true);
@@ -1122,6 +1323,11 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
     bld.begin_phase(P.lmul);
     bld.lmul(0, Z);
     bld.end_phase();
+    for (const auto& a : bld.tmps)
+        if (a.refs != 0) throw std::logic_error("planner: live temporary at the end of planning");
+    P.arena_off = bld.arena_base;
+    P.arena_size = bld.arena_top;
+    bld.bump = bld.arena_base + bld.arena_top;
     // place the ring and rebase every truncation workspace offset onto it
     P.ring_size = bld.ring_nchunks * bld.ring_chunk;
     P.ring_off = bld.alloc(P.ring_size);
@@ -1129,9 +1335,12 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max) {
         for (TTask& t : ph->tt) t.ws += P.ring_off;
     P.pool_total = bld.bump;
     if (std::getenv("HM_PLAN_VERBOSE"))
-        std::fprintf(stderr, "plan: blocks(C~ at capacity)=%.3f GB z=%.3f GB tmp=%.3f GB ring=%.3f GB other temporaries=%.3f GB total=%.3f GB\n",
+        std::fprintf(stderr, "plan: blocks(C~ at capacity)=%.3f GB z=%.3f GB tmp=%.3f GB ring=%.3f GB arena=%.3f GB total=%.3f GB\n",
                      8e-9 * P.bytes_C / 8, 8e-9 * (double)T.n * P.zw, 8e-9 * 8192 * 4096.0, 8e-9 * P.ring_size,
-                     8e-9 * (P.pool_total - P.pool_blocks - 8192 * 4096.0 - P.ring_size), 8e-9 * P.pool_total);
+                     8e-9 * P.arena_size, 8e-9 * P.pool_total);
+    if (std::getenv("HM_PLAN_VERBOSE"))
+        std::fprintf(stderr, "temporaries allocated: push_down %.3f GB, eval_pieces %.3f GB, cores %.3f GB\n",
+                     1e-9 * bld.site_bytes[1], 1e-9 * bld.site_bytes[2], 1e-9 * bld.site_bytes[3]);
 }
 
 }  // namespace hm

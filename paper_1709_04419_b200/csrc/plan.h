@@ -41,6 +41,7 @@ struct Thin {
     int32_t cols = 0;            // static (maximum) number of columns
     int32_t slot = -1;           // rank slot giving the actual column count (-1: static)
     int32_t res0 = -1;           // resource id of the chunk of the first leaf of `cluster`
+    int32_t tmp = -1;            // temporary-arena allocation it lives in (-1: permanent storage)
 };
 
 struct Phase {                   // one executable phase (levelled task lists)
@@ -78,6 +79,7 @@ struct Plan {
     int64_t bytes_C = 0;               // bytes of block storage at capacity
     int64_t ring_off = 0, ring_size = 0;  // truncation workspace ring (doubles)
     int64_t tmp_off = 0;                  // ring of 64 x 64 temporary tiles (split dense updates)
+    int64_t arena_off = 0, arena_size = 0;   // temporaries of the H x thin products (liveness-planned)
     // assembly
     std::vector<DenseGenTask> dgen;
     std::vector<AcaTask> aca;
@@ -96,6 +98,9 @@ constexpr int32_t TILE_MAX_LEAF = 64;
 
 // Build the full plan for a tree (any n >= 1, any leaf size the storage refinement can
 // halve down to TILE_MAX_LEAF without empty clusters).
-void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max = TR_COOP_DEFAULT);
+// arena_budget: doubles the H x thin temporaries may occupy before recycling memory
+// whose last users finish late (longer critical path, smaller footprint).
+void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max = TR_COOP_DEFAULT,
+                int64_t arena_budget = INT64_MAX);
 
 }  // namespace hm

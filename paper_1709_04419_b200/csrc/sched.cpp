@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "api_util.h"
 
@@ -98,6 +100,15 @@ void build_sched(const Phase& p, Sched& s) {
     }
     for (int i = 0; i < nx; ++i)
         if (node[i] == i) bmax = std::max(bmax, bl[i]);
+    if (std::getenv("HM_PLAN_VERBOSE")) {
+        double work = 0.0;
+        for (int i = 0; i < nx; ++i) {
+            const XTask& x = p.xt[i];
+            work += (x.kind == 0) ? vm_cost(p, p.vt[x.idx]) : tr_cost(p.tt[x.idx], x.nsub);
+        }
+        std::fprintf(stderr, "sched: %d tasks, critical path %.1f ms, work %.1f CTA-ms (model)\n", nx, 1e-3 * bmax,
+                     1e-3 * work);
+    }
     // priority level -> queue; count slots per queue
     std::vector<int32_t> cnt(RQ_NQ, 0);
     for (int i = 0; i < nx; ++i) {
