@@ -81,6 +81,12 @@ def theta_schedule(w, steps):
     return out
 
 
+def rank_thetas(w, steps, S, rank, world):
+    """The thetas rank `rank` evaluates: every rank walks its own slice of one global
+    schedule (round-robin, steps * S each; independent evaluations, no collective)."""
+    return theta_schedule(w, steps * world * S)[rank::world]
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -156,6 +162,32 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------- reference (oracle) arm
+def oracle_sample(w, th):
+    """One oracle evaluation (dense Eq. 1, CPU fp64, oracle/ as it stands) on a bounded
+    sub-sample of n_s workload points, timed in its two parts: the dense covariance
+    (O(n^2) K_nu evaluations) and the Cholesky + solve (O(n^3)).  Returns
+    (seconds assembly, seconds factorisation, n_s)."""
+    from oracle import dense as od
+    from synthetic import standard_normal
+    n_s = min(int(os.environ.get("HM_REF_SAMPLE_N", "3000")), w["n"])
+    pts = make_points(w)
+    rng = np.random.default_rng(5)
+    sub = pts[np.sort(rng.choice(w["n"], size=n_s, replace=False))]
+    Z = standard_normal(n_s, 1, 7)[:, 0]
+    t0 = time.perf_counter()
+    C = od.covariance(sub, th, bessel="scipy")
+    t1 = time.perf_counter()
+    od.loglik_from_cov(C, Z)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, n_s
+
+
+def extrapolate(ta, tc, n_s, n):
+    """Seconds of one oracle evaluation at the workload's n: assembly scaled by (n/n_s)^2,
+    factorisation + solve by (n/n_s)^3 (the dense algorithm's own complexities)."""
+    return ta * (n / n_s) ** 2 + tc * (n / n_s) ** 3
+
+
 def run_reference(args, w):
     ws, rk, lr = dist_env()
     if ws > 1:
@@ -165,33 +197,35 @@ def run_reference(args, w):
             dist.barrier()
             dist.destroy_process_group()
             return
-    from oracle import dense as od
-    from synthetic import standard_normal, uniform_iid
-    # bounded sample: dense Eq. (1) at n_s points of the workload's distribution,
-    # scaled to the workload's n by the dense O(n^3) cost (the oracle is dense).
-    n_s = min(int(os.environ.get("HM_REF_SAMPLE_N", "3000")), w["n"])
-    pts = make_points(w)
-    rng = np.random.default_rng(5)
-    sub = pts[np.sort(rng.choice(w["n"], size=n_s, replace=False))]
-    Z = standard_normal(n_s, 1, 7)[:, 0]
     ths = theta_schedule(w, args.warmup + args.steps)
     for s in range(args.warmup):
-        od.loglik(sub, Z, ths[s], bessel="scipy")
+        oracle_sample(w, ths[s])
+    ta = tc = 0.0
     t0 = time.perf_counter()
     for s in range(args.steps):
-        od.loglik(sub, Z, ths[args.warmup + s], bessel="scipy")
-    dt = (time.perf_counter() - t0) / args.steps
-    scale = (n_s / w["n"]) ** 3
-    value = scale / dt
+        a, c, n_s = oracle_sample(w, ths[args.warmup + s])
+        ta += a
+        tc += c
+    wall = (time.perf_counter() - t0) / args.steps
+    ta, tc = ta / args.steps, tc / args.steps
+    t_n = extrapolate(ta, tc, n_s, w["n"])
+    value = 1.0 / t_n
     cores = len(os.sched_getaffinity(0))
     line = {"metric": f"H-log-likelihood evals/sec at n={w['n']}", "value": value, "unit": "evals/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": workload_str(w, args), "oracle_sample_n": n_s},
+            "config": {"workload": workload_str(w, args), "oracle_sample_n": n_s,
+                       "step": f"one dense oracle evaluation at n_s={n_s} points of the workload "
+                               f"(measured {1e3 * wall:.0f} ms = ms_per_step)",
+                       "extrapolation": f"value = 1 / (t_asm (n/n_s)^2 + t_chol (n/n_s)^3) with t_asm = {ta:.3f} s, "
+                                        f"t_chol = {tc:.3f} s measured at n_s: {t_n:.0f} s per evaluation at "
+                                        f"n = {w['n']} (not run: {8 * w['n'] ** 2 / 1e9:.0f} GB dense matrix)"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                             "sample": f"dense Eq.(1) oracle at n={n_s} ({dt:.2f} s/eval), scaled by (n_s/n)^3"},
-            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"dense Eq.(1) oracle at n_s={n_s}, assembly scaled by (n/n_s)^2, "
+                                       f"Cholesky + solve by (n/n_s)^3"},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "paper_cpu_context": paper_context(w)}
     print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -200,27 +234,26 @@ def run_reference(args, w):
 
 
 def cpu_baseline(w, budget_s=20.0):
-    """Oracle (dense Eq. 1, CPU fp64) timed on a bounded sample; evals/s scaled to n."""
-    from oracle import dense as od
-    from synthetic import standard_normal
-    pts = make_points(w)
-    n_s = min(int(os.environ.get("HM_REF_SAMPLE_N", "3000")), w["n"])
-    rng = np.random.default_rng(5)
-    sub = pts[np.sort(rng.choice(w["n"], size=n_s, replace=False))]
-    Z = standard_normal(n_s, 1, 7)[:, 0]
+    """The oracle (dense Eq. 1, CPU fp64) on a bounded sample, extrapolated to the
+    workload's n with the dense algorithm's own complexities (see extrapolate)."""
     th = w["thetas"][0]
+    oracle_sample(w, th)                     # warm (imports, scipy)
     t0 = time.perf_counter()
+    ta = tc = 0.0
     reps = 0
     while True:
-        od.loglik(sub, Z, th, bessel="scipy")
+        a, c, n_s = oracle_sample(w, th)
+        ta += a
+        tc += c
         reps += 1
         if time.perf_counter() - t0 > budget_s / 2 or reps >= 5:
             break
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": (n_s / w["n"]) ** 3 / dt, "unit": "evals/s", "cores": len(os.sched_getaffinity(0)),
+    ta, tc = ta / reps, tc / reps
+    return {"value": 1.0 / extrapolate(ta, tc, n_s, w["n"]), "unit": "evals/s", "cores": len(os.sched_getaffinity(0)),
             "kind": "oracle",
-            "sample": f"{reps} dense Eq.(1) oracle evals at n={n_s} sub-sampled from the workload "
-                      f"({dt:.2f} s each), scaled to n={w['n']} by (n_s/n)^3"}
+            "sample": f"{reps} dense Eq.(1) oracle evals at n_s={n_s} sub-sampled from the workload "
+                      f"(assembly {ta:.2f} s, Cholesky + solve {tc:.2f} s each), extrapolated to n={w['n']} "
+                      f"by (n/n_s)^2 and (n/n_s)^3"}
 
 
 # ---------------------------------------------------------------------------- GPU arm
@@ -237,11 +270,11 @@ def run_mc(args, w):
     from paper_1709_04419_b200.mle import mc_mle
     S = max(1, args.theta_streams)
     sms = torch.cuda.get_device_properties(lr).multi_processor_count
-    strs = [torch.cuda.Stream(device=lr) for _ in range(S)] if S > 1 else None
-    handles = [x.cuda_stream for x in strs] if strs else None
-    # warm-up replicates (untimed), then args.steps * S replicates per rank, timed (S co-scheduled)
+    reps = args.replicates or ws * args.steps * S
+    # warm-up replicates (untimed), then `reps` replicates over all ranks, timed; each rank
+    # fits its replicates S at a time (lockstep Nelder-Mead, one hm_loglik_multi per round)
     mc_mle(w["n"], ws * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"], leaf=w["leaf"],
-           rank=rk, world=ws, device=lr, seed=10_000, gather=False, streams=handles, sms=sms, kmax=args.kmax)
+           rank=rk, world=ws, device=lr, seed=10_000, gather=False, streams=S, sms=sms, kmax=args.kmax)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -249,8 +282,8 @@ def run_mc(args, w):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(lr) as clk:
         e0.record(stream)
-        res = mc_mle(w["n"], ws * args.steps * S, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
-                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False, streams=handles, sms=sms,
+        res = mc_mle(w["n"], reps, w["thetas"][0], w["start"], eps=w["eps"], evals=w["evals"],
+                     leaf=w["leaf"], rank=rk, world=ws, device=lr, seed=0, gather=False, streams=S, sms=sms,
                      kmax=args.kmax)
         torch.cuda.synchronize()
         e1.record(stream)
@@ -261,12 +294,13 @@ def run_mc(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     if rk == 0:
-        n_evals = ws * args.steps * S * w["evals"]
+        n_evals = reps * w["evals"]
         line = {"metric": f"H-log-likelihood evals/sec (MC-MLE, n={w['n']})", "value": n_evals / (ms / 1e3),
                 "unit": "evals/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_str(w, args),
+                           "replicates": reps,
                            "step": f"{S} replicate(s) per rank (incl. their H-build and sampler)",
                            "parallelism": f"replicas x{ws}; {S} co-scheduled replicates per GPU"},
                 "estimates_rank0": res.tolist(), "clocks": clk.summary()}
@@ -275,14 +309,40 @@ def run_mc(args, w):
         dist.destroy_process_group()
 
 
+def paper_context(w):
+    """PAPER.md Table 3 (l.483-500): HLIBpro on 40 cores (Dell workstation, 20
+    processors, 128 GB, l.210), eps = 1e-5 for C~ and L~, theta = (0.98, 0.64, 0.325)
+    on soil-moisture locations -- context, not a target (other machine, other data)."""
+    rows = {64000: (5.3, 5.1), 2000000: (227.0, 471.0), 128000: (13.2, 13.7), 32000: (3.2, 2.3)}
+    n = min(rows, key=lambda r: abs(r - w["n"]))
+    c, l = rows[n]
+    return {"source": "PAPER.md Table 3 (l.494-500)", "n": n, "C_build_s": c, "cholesky_s": l,
+            "evals_per_s_equiv": 1.0 / (c + l), "cores": 40,
+            "hardware": "Dell workstation, 20 processors (40 cores), 128 GB RAM (PAPER.md l.210)",
+            "eps": 1e-5, "theta": [0.98, 0.64, 0.325]}
+
+
+def traffic_of(kernel_key, workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    summary (profiles/traffic.json, written from the capture), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    e = d.get(workload, {}).get(kernel_key)
+    if not e:
+        return None, None
+    return e["dram_bytes_per_launch"], e["source"]
+
+
 def run_gpu(args, w):
-    """configs[2]-style throughput: each rank evaluates its own theta sequence.  On one
-    GPU, S handles (same locations, own factor storage) run side by side, each on its
-    own CUDA stream and host thread with 1/S of the SMs for its persistent executor
-    (hm_set_exec_grid): a step is S complete, independent likelihood evaluations
-    (assemble + H-Cholesky + solve each).  --theta-streams 1 is the single-evaluation
-    latency configuration."""
-    import threading
+    """configs[2]-style throughput through the C-ABI's batched entry point: each rank
+    evaluates its own theta sequence with hm_loglik_batch, S thetas per call; inside
+    the library S executors (the handle + S - 1 siblings on the same tree and plan)
+    run the evaluations co-scheduled on the GPU, each persistent executor capped at
+    1/S of the SMs (include/hmlik.h).  A step = one hm_loglik_batch call = S complete,
+    independent likelihood evaluations (assemble + H-Cholesky + solve each).  The
+    single-evaluation latency (S = 1) is measured in the same run."""
     import torch
     ws, rk, lr = dist_env()
     torch.cuda.set_device(lr)
@@ -291,95 +351,79 @@ def run_gpu(args, w):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     import paper_1709_04419_b200 as hm
+    from paper_1709_04419_b200.dist import gather_results
     from synthetic import standard_normal
 
     S = max(1, args.theta_streams)
     sms = torch.cuda.get_device_properties(lr).multi_processor_count
-    caps = [sms // S + (1 if i < sms % S else 0) for i in range(S)] if S > 1 else [0]
     # cooperative groups <= 8 CTAs when co-scheduled, and within the deadlock bound
-    # 4 * (coop - 1) < executor CTAs (hm_set_exec_grid)
-    coop = 16 if S == 1 else max(1, min(8, (min(caps) - 1) // 4 + 1))
+    # 4 * (coop - 1) < executor CTAs = sms / S
+    coop = 16 if S == 1 else max(1, min(8, (sms // S - 1) // 4 + 1))
     pts = make_points(w)
     n = pts.shape[0]
     steps, warm = args.steps, args.warmup
-    # each (rank, stream) walks its own theta sequence (independent evaluations)
-    ths_all = theta_schedule(w, (warm + steps) * ws * S)
-    seqs = [ths_all[rk * S + i::ws * S] for i in range(S)]
-    streams = [torch.cuda.Stream(device=lr) for _ in range(S)]
-    Hs = []
-    for i in range(S):
-        H = hm.HMatrix(pts, seqs[i][0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=args.kmax, device=lr,
-                       stream=streams[i].cuda_stream, coop_max=coop)
-        H.set_exec_grid(caps[i])
-        Hs.append(H)
-    Hs[0].cholesky()
+    mine = rank_thetas(w, warm + steps, S, rk, ws)   # this rank's thetas, S per step
+    H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=args.kmax, device=lr,
+                   coop_max=coop)
+    H.cholesky()
     xi = standard_normal(n, 1, 11)
-    Zh = np.asfortranarray(Hs[0].sample(xi))
-    Zd = torch.from_numpy(np.ascontiguousarray(Zh[:, 0])).to(f"cuda:{lr}")
+    Zh = np.ascontiguousarray(H.sample(xi)[:, 0])
+    Zd = torch.from_numpy(Zh).to(f"cuda:{lr}")
+    H.set_batch_streams(S)
     torch.cuda.synchronize()
 
-    def step(H, th, Z):
-        H.assemble(th)
-        H.cholesky()
-        return H.loglik(Z)
+    def batch(s, Z):
+        out, rc = H.loglik_batch(mine[s * S:(s + 1) * S], Z)
+        hm._binding.check(rc)
+        return out
 
-    def run_all(first, count, Z, outs):
-        def worker(i):
-            for s_ in range(first, first + count):
-                outs[i].append(step(Hs[i], seqs[i][s_], Z)[0].copy())
-        th = [threading.Thread(target=worker, args=(i,)) for i in range(S)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-
-    run_all(0, warm, Zd, [[] for _ in range(S)])
+    for s in range(warm):
+        batch(s, Zd)
     if not args.no_profile:
-        for H in Hs:
-            H.profile(True)
+        H.profile(True)
 
-    def timed(Z):
-        outs = [[] for _ in range(S)]
+    def timed(Z, first, count):
+        outs = []
+        cur = torch.cuda.current_stream()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(streams[0])
-        run_all(warm, steps, Z, outs)
-        e1 = []
-        for st in streams:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(st)
-            e1.append(e)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for s in range(first, first + count):
+            outs.append(batch(s, Z))      # synchronous: returns when its S evaluations are done
+        e1.record(cur)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        return max(e0.elapsed_time(e) for e in e1), outs
+        return e0.elapsed_time(e1), outs
 
     with ClockSampler(lr) as clk:
-        ms, outs = timed(Zd)
-    kst = [H.kernel_stats() for H in Hs]
-    for H in Hs:
-        H.profile(False)
-    kstats = {}
-    for k in kst[0]:
-        kstats[k] = {f: sum(x[k][f] for x in kst) for f in kst[0][k]}
+        ms, outs = timed(Zd, warm, steps)
+    kstats = H.kernel_stats()
+    H.profile(False)
     launches = int(sum(v["launches"] for v in kstats.values()))
-    # end-to-end through the C-ABI with HOST buffers: per evaluation the host Z goes
-    # h2d and the (loglik, logdet, quad) triple comes back d2h
-    Zp = torch.from_numpy(np.ascontiguousarray(Zh[:, 0])).pin_memory()   # pinned host input
-    ms_e2e, _ = timed(Zp)
+    # end-to-end through the C-ABI with HOST data: every evaluation copies Z h2d and
+    # its (loglik, logdet, quad) triple d2h
+    ms_e2e, _ = timed(Zh, warm, steps)
+    # single-evaluation latency (one executor on the whole GPU, same plan)
+    H.set_batch_streams(1)
+    lat_n = min(steps, 6) * S
+    lat_ms, _ = timed(Zd, warm, lat_n // S)
+    H.set_batch_streams(S)
+    res = np.concatenate([o.reshape(-1, 3) for o in outs])       # this rank's (loglik, logdet, quad)
+    allres = gather_results(res, len(res) * ws, rk, ws, device=f"cuda:{lr}") if dist else res
     if dist:
-        t = torch.tensor([ms, ms_e2e], device=f"cuda:{lr}", dtype=torch.float64)
+        t = torch.tensor([ms, ms_e2e, lat_ms], device=f"cuda:{lr}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_e2e = t.tolist()
-    st = Hs[0].stats()
+        ms, ms_e2e, lat_ms = t.tolist()
+    st = H.stats()
     if rk == 0:
         ev = ws * steps * S
         value = ev / (ms / 1e3)
         peaks = load_peaks()
-        roof = roofline(kstats, peaks)
+        roof = roofline(kstats, peaks, w)
         if roof is not None:
             roof["concurrent_launches"] = S
             roof["aggregate_achieved"] = (kstats["k_exec"]["flops"] / 1e12) / (ms / 1e3) if "k_exec" in kstats else None
@@ -388,12 +432,13 @@ def run_gpu(args, w):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_str(w, args),
                            "l2": "no flush: H-matrix storage > 126 MB L2",
-                           "parallelism": f"replicas x{ws}; {S} co-scheduled theta streams per GPU "
-                                          f"(executor CTAs {caps if S > 1 else sms}, coop_max {coop}); "
-                                          f"a step = {S} independent evaluations per GPU",
-                           "evals_per_step": ev,
+                           "parallelism": f"replicas x{ws}; hm_loglik_batch with {S} co-scheduled executors per GPU "
+                                          f"(persistent executor CTAs {sms // S} each, coop_max {coop})",
+                           "evals_per_step_per_gpu": S, "evals_timed_total": ev,
                            "max_rank_C": st["max_rank_C"], "max_rank_L": st["max_rank_L"],
                            "bytes_L_MB": round(st["bytes_L"] / 2**20, 1)},
+                "latency": {"ms_per_eval": lat_ms / lat_n, "evals_per_s": lat_n / (lat_ms / 1e3),
+                            "how": f"{lat_n} evaluations one at a time (hm_set_batch_streams 1), whole GPU"},
                 "e2e": {"value": ev / (ms_e2e / 1e3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n * S,
                         "d2h_bytes_per_step": 24 * S},
                 "gpu_launches": launches,
@@ -401,26 +446,29 @@ def run_gpu(args, w):
                 "kernels": {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["ms"] / steps,
                                 "share": v["ms"] / max(1e-9, sum(x["ms"] for x in kstats.values()))}
                             for k, v in kstats.items()},
-                "loglik_first": outs[0][0].tolist(),
+                "results": {"gathered": int(allres.shape[0]), "loglik_first": allres[0].tolist(),
+                            "finite": bool(np.isfinite(allres).all())},
+                "paper_cpu_context": paper_context(w),
                 "clocks": clk.summary()}
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(line), flush=True)
-    for H in Hs:
-        H.close()
+    H.close()
     if dist:
         dist.destroy_process_group()
 
 
-def roofline(kstats, peaks):
+def roofline(kstats, peaks, w):
     """Dominant kernel (largest device time in the timed region) against its bound."""
     if not kstats:
         return None
     name, v = max(kstats.items(), key=lambda kv: kv[1]["ms"])
     if v["ms"] <= 0.0:
         return None
+    key = name
     if name == "k_exec":   # the family's kernel in the default execution mode (ready queues)
         name = "k_exec_rq (persistent executor: recompression, H-Cholesky, solve launches averaged)"
+    traffic, tsrc = traffic_of(key, w["cfg"])
     per_launch_s = v["ms"] / 1e3 / max(1, v["launches"])
     flops = v["flops"] / max(1, v["launches"])
     byts = v["bytes"] / max(1, v["launches"])
@@ -429,11 +477,13 @@ def roofline(kstats, peaks):
     if t_f >= t_b:
         ach = flops / per_launch_s / 1e12
         return {"kernel": name, "bound": "fp64", "achieved": ach, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                "frac": ach / peaks["fp64_tflops"], "traffic": None, "algorithmic_flops_per_launch": flops,
+                "frac": ach / peaks["fp64_tflops"], "traffic": traffic, "traffic_src": tsrc,
+                "algorithmic_flops_per_launch": flops,
                 "algorithmic_bytes_per_launch": byts, "peak_src": peaks["fp64_src"]}
     ach = byts / per_launch_s / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_flops_per_launch": flops,
+            "frac": ach / peaks["hbm_gbs"], "traffic": traffic, "traffic_src": tsrc,
+            "algorithmic_flops_per_launch": flops,
             "algorithmic_bytes_per_launch": byts, "peak_src": peaks["hbm_src"]}
 
 
@@ -448,12 +498,24 @@ def main():
                     help="rank capacity per low-rank block (ranks at the workloads' eps stay <= 30; HM_ERR_RANK_CAP if exceeded)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch CUDA events (kernel table empty)")
+    ap.add_argument("--replicates", type=int, default=0,
+                    help="--workload mc: replicates in the timed region (0 = gpus * steps * theta-streams; "
+                         "configs[3] is 128)")
     ap.add_argument("--theta-streams", type=int, default=4,
                     help="independent theta evaluations co-scheduled per GPU (1 = single-evaluation latency)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     w = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun (the driver launches
+        # it that way itself; this makes `bench.py --gpus N` do the same)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29517"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args, w)
     elif args.workload == "mc":

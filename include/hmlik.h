@@ -68,7 +68,9 @@ typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
  * eps_chol: accuracy of every truncation inside the H-Cholesky (same meaning
  * as eps; 0 = eps).  The paper fixes the accuracies of C~ and L~ separately
  * (l.474-476, Fig. 7: 1e-3 for C~, 1e-8 for L~); Table 3 (l.483) uses one for
- * both, which is the default.                                                 */
+ * both, which is the default.  exec_ctas: CTA cap of the handle's persistent
+ * executor from hm_build on (0 = all SMs; as hm_set_exec_grid), so a handle built
+ * while other handles' executors run never oversubscribes the SMs.             */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
@@ -77,6 +79,7 @@ typedef struct hm_params {
     int32_t rel_eps;
     int32_t coop_max;
     double  eps_chol;
+    int32_t exec_ctas;
 } hm_params;
 
 typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */
@@ -139,12 +142,39 @@ int hm_cholesky(hm_handle h);
  * j, written to host memory.  Requires hm_cholesky first (HM_ERR_STATE).    */
 int hm_loglik(hm_handle h, const double* Z, int32_t z_on_device, int32_t k, double* out_host);
 
-/* One full evaluation per theta: for each of n_theta thetas, assemble +
- * Cholesky + loglik for the k columns of Z.  out: n_theta x k x 3 (host).
- * Failed factorizations store (-inf, nan, nan) for that theta and continue;
- * the return value is the first error seen (HM_OK if none).                 */
+/* One full evaluation per theta (Eq. 4 at each theta of a grid, an optimiser's
+ * simplex, Monte-Carlo draws): for each of n_theta thetas, assemble + Cholesky
+ * + loglik for the k columns of Z (n x k, host or device; device data must be
+ * complete before the call).  out: n_theta x k x 3 (host), out[3k*i + 3c + ...].
+ * The evaluations are co-scheduled on the handle's GPU: S executors (the handle
+ * and S - 1 sibling handles on the same tree and plan, each with its own device
+ * storage and stream, created on first use and kept) run concurrently from S host
+ * threads, each persistent executor capped at 1/S of the SMs.  S is the value of
+ * hm_set_batch_streams (default 4), reduced to what the plan's cooperative
+ * truncation groups allow (each executor needs more than 4 * (largest group - 1)
+ * CTAs; hm_params.coop_max = 8 allows 4), to n_theta, and to what fits in device
+ * memory.  Results are bit-identical to evaluating the thetas one at a time (the
+ * CTA cap never changes the arithmetic).  Failed evaluations store
+ * (-inf, nan, nan) for that theta and the rest continue; the return value is the
+ * first error seen (HM_OK if none).  Afterwards the handle holds no factor
+ * (hm_assemble again before hm_cholesky / hm_loglik).                        */
 int hm_loglik_batch(hm_handle h, const hm_theta* thetas_host, int32_t n_theta,
                     const double* Z, int32_t z_on_device, int32_t k, double* out_host);
+
+/* Co-scheduled evaluations on DIFFERENT handles (e.g. Monte-Carlo replicates,
+ * each on its own locations, sec. 4): handle i is assembled at
+ * thetas[i], factored, and evaluated on its own data Zs[i] (n_i x k, host or
+ * device), concurrently, one host thread per handle, the executors splitting the
+ * SMs (each must keep more than 4 * (largest cooperative group - 1) CTAs, else
+ * HM_ERR_ARG).  All handles on one device, none twice.  out: nh x k x 3 (host);
+ * errors as in hm_loglik_batch.                                               */
+int hm_loglik_multi(int32_t nh, const hm_handle* handles, const hm_theta* thetas_host,
+                    const double* const* Zs, int32_t z_on_device, int32_t k, double* out_host);
+
+/* Number of co-scheduled executors hm_loglik_batch may use (0 = default 4,
+ * 1 = one evaluation at a time, at most 16).  Lowering it frees the surplus
+ * sibling handles' device memory.  HM_ERR_ARG outside [0, 16].               */
+int hm_set_batch_streams(hm_handle h, int32_t streams);
 
 /* Sampler (sec. 4, l.308 "Z = L~ xi"): Z = L~ xi for k standard-normal
  * columns xi (n x k, original order, host or device); Z written in original
@@ -164,8 +194,8 @@ int hm_timings(hm_handle h, double ms[3]);
 
 /* Profiling (measurement support, bench.py).  hm_profile(h, 1) resets the
  * per-kernel accumulators and brackets every subsequent kernel launch of the
- * handle with a CUDA event pair on the handle's stream; hm_profile(h, 0)
- * stops recording.  Both synchronise the handle's stream.                   */
+ * handle (and of its hm_loglik_batch siblings) with a CUDA event pair on its
+ * stream; hm_profile(h, 0) stops recording.  Both synchronise the streams.  */
 int hm_profile(hm_handle h, int32_t enable);
 
 /* Execution mode of the planned phases (Cholesky, solve, sampler, recompression):
@@ -213,7 +243,8 @@ int hm_checksum(hm_handle h, double out[4]);
  * n > HM_DENSE_NMAX.                                                         */
 int hm_to_dense(hm_handle h, double* out_host);
 
-/* Per kernel family f = 0..5 (dense Matern block generation, ACA, low-rank
+/* Summed over the handle and its hm_loglik_batch siblings: per kernel family
+ * f = 0..5 (dense Matern block generation, ACA, low-rank
  * truncation, tile VM, auxiliary gather/finish, persistent executor -- whose
  * flops/bytes are those of the truncation + VM tasks it ran): out[4f + 0] launches since
  * the last hm_profile, out[4f + 1] summed device milliseconds of those

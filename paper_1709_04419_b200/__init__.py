@@ -4,6 +4,6 @@ Public Python API = thin wrappers over the C-ABI in include/hmlik.h:
 ``Tree``, ``HMatrix`` (hm_build / hm_cholesky / hm_loglik / ...),
 ``dense_loglik`` (GPU dense check path), ``matern_block``.
 """
-from ._binding import (HMError, HMatrix, Tree, dense_loglik, matern_block, lib)  # noqa: F401
+from ._binding import (HMError, HMatrix, Tree, dense_loglik, loglik_multi, matern_block, lib)  # noqa: F401
 
-__all__ = ["HMError", "HMatrix", "Tree", "dense_loglik", "matern_block", "lib"]
+__all__ = ["HMError", "HMatrix", "Tree", "dense_loglik", "loglik_multi", "matern_block", "lib"]

@@ -31,7 +31,8 @@ class Theta(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32),
-                ("rel_eps", C.c_int32), ("coop_max", C.c_int32), ("eps_chol", C.c_double)]
+                ("rel_eps", C.c_int32), ("coop_max", C.c_int32), ("eps_chol", C.c_double),
+                ("exec_ctas", C.c_int32)]
 
 
 def _load():
@@ -66,6 +67,8 @@ def _load():
         "hm_trace": ([P, I32, C.c_char_p], C.c_int),
         "hm_checksum": ([P, P], C.c_int),
         "hm_to_dense": ([P, P], C.c_int),
+        "hm_loglik_multi": ([I32, P, P, P, I32, I32, P], C.c_int),
+        "hm_set_batch_streams": ([P, I32], C.c_int),
         "hm_dense_loglik": ([P, I32, I64, Theta, P, I32, I32, I32, P, P], C.c_int),
         "hm_matern_block": ([P, I64, P, I64, Theta, I32, P], C.c_int),
     }
@@ -80,7 +83,7 @@ lib = _load()
 EXPORTED = ("hm_last_error", "hm_version", "hm_tree_build", "hm_tree_free", "hm_tree_counts", "hm_tree_perm",
             "hm_tree_clusters", "hm_tree_blocks", "hm_plan_dump", "hm_build", "hm_free", "hm_assemble", "hm_cholesky",
             "hm_loglik", "hm_loglik_batch", "hm_sample", "hm_stats", "hm_timings", "hm_profile",
-            "hm_kernel_stats", "hm_set_exec_mode", "hm_set_exec_grid", "hm_trace", "hm_checksum", "hm_to_dense",
+            "hm_kernel_stats", "hm_set_exec_mode", "hm_set_exec_grid", "hm_trace", "hm_checksum", "hm_to_dense", "hm_loglik_multi", "hm_set_batch_streams",
             "hm_dense_loglik", "hm_matern_block")
 
 
@@ -187,6 +190,28 @@ def matern_block(a, b, theta, device: int = 0) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- H-matrix likelihood
+def loglik_multi(handles, thetas, Zs):
+    """hm_loglik_multi: handle i at thetas[i] on its own data Zs[i], all co-scheduled on
+    one GPU.  Returns (len(handles) x k x 3 array, status code)."""
+    nh = len(handles)
+    keep = [_zarg(Z) for Z in Zs]
+    ks = {kp[3] for kp in keep}
+    devs = {kp[1] for kp in keep}
+    if len(ks) != 1 or len(devs) != 1:
+        raise ValueError("all data must have the same column count and location (host / device)")
+    for H, kp, Z in zip(handles, keep, Zs):
+        H._check_rows(kp[2], Z)
+    k = ks.pop()
+    hs = (C.c_void_p * nh)(*[H._h.value for H in handles])
+    zp = (C.c_void_p * nh)(*[kp[0].value for kp in keep])
+    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(nh, 3))
+    out = np.empty((nh, k, 3))
+    rc = lib.hm_loglik_multi(nh, hs, th.ctypes.data_as(C.c_void_p), zp, devs.pop(), int(k),
+                             out.ctypes.data_as(C.c_void_p))
+    return out, rc
+
+
+
 def _zarg(Z):
     """(pointer, on_device, n, k, keepalive) for data vectors: numpy n / n x k, or torch (n,) / (k, n)."""
     if isinstance(Z, np.ndarray) or not hasattr(Z, "is_cuda"):
@@ -207,7 +232,8 @@ class HMatrix:
     """
 
     def __init__(self, locs, theta, eps: float = 1e-8, leaf: int = 32, eta: float = 2.0, kmax: int = 160,
-                 device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0, eps_chol: float = 0.0):
+                 device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0, eps_chol: float = 0.0,
+                 exec_ctas: int = 0):
         if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
             locs = _as_f64(locs)
         lp, ld = ptr_of(locs)
@@ -215,7 +241,7 @@ class HMatrix:
         self.device = int(device)
         self._h = C.c_void_p()
         self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0, int(coop_max),
-                             float(eps_chol))
+                             float(eps_chol), int(exec_ctas))
         rc = lib.hm_build(lp, ld, self.n, Theta(*theta), self.params, int(device),
                           C.c_void_p(stream) if stream else None, C.byref(self._h))
         check(rc)
@@ -247,6 +273,10 @@ class HMatrix:
         rc = lib.hm_loglik_batch(self._h, th.ctypes.data_as(C.c_void_p), th.shape[0], p, d, int(k),
                                  out.ctypes.data_as(C.c_void_p))
         return out, rc
+
+    def set_batch_streams(self, streams: int):
+        """Co-scheduled executors of loglik_batch (0 = default 4, 1 = sequential)."""
+        check(lib.hm_set_batch_streams(self._h, int(streams)))
 
     def sample(self, xi) -> np.ndarray:
         p, d, n, k, keep = _zarg(xi)

@@ -8,7 +8,11 @@
 // truncation kernel for its truncation tasks.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -82,6 +86,9 @@ struct hm_handle_s {
     size_t pin_z_n = 0;
     double* pin_out = nullptr;
     size_t pin_out_n = 0;
+    // hm_loglik_batch: S - 1 sibling executors on the same tree + plan (own pool, stream)
+    std::vector<std::unique_ptr<hm_handle_s>> subs;
+    int batch_streams = 0;   // 0 = auto (hm_set_batch_streams)
     ~hm_handle_s() {
         if (pin_z) cudaFreeHost(pin_z);
         if (pin_out) cudaFreeHost(pin_out);
@@ -331,6 +338,144 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
     h->ms[2] = elapsed(h);
 }
 
+// Device side of a handle whose tree and plan are built: pool, task lists, schedules.
+void setup_device(hm_handle_s* h) {
+    vm_set_attr();
+    h->pool.alloc(sizeof(double) * (size_t)std::max<int64_t>(h->P.pool_total, 1));
+    upload(h->pts, h->T.pts, h->stream);
+    upload(h->perm, h->T.perm, h->stream);
+    h->ranks.alloc(sizeof(int) * (h->P.n_slots + 1));
+    HM_CUDA_TRY(cudaMemsetAsync(h->ranks.p, 0, sizeof(int) * (h->P.n_slots + 1), h->stream));
+    h->flags.alloc(sizeof(int) * 4);
+    h->ctr.alloc(sizeof(double) * CTR_N);
+    {
+        size_t mx = 1;
+        for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) mx = std::max(mx, ph->xt.size());
+        h->done.alloc(sizeof(int) * mx);
+        HM_CUDA_TRY(cudaMemsetAsync(h->done.p, 0, sizeof(int) * mx, h->stream));
+        h->counter.alloc(sizeof(int) * 4);
+        h->rq_cnt.alloc(sizeof(int) * mx);
+        h->rq_slot.alloc(sizeof(int) * mx);
+        h->rq_ctl.alloc(sizeof(int) * (2 * RQ_NQ + 2));
+        int nb = 1;
+        for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) nb = std::max(nb, ph->n_bars);
+        h->bars.alloc(sizeof(int) * nb);
+        exec_grid();
+        exec_grid_rq();
+    }
+    HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
+    h->out.alloc(sizeof(double) * 3 * h->P.zw);
+    upload(h->dgen, h->P.dgen, h->stream);
+    upload(h->aca, h->P.aca, h->stream);
+    upload_phase(h->rec, h->P.recompress, h->stream);
+    upload_phase(h->chol, h->P.chol, h->stream);
+    upload_phase(h->solve, h->P.solve, h->stream);
+    upload_phase(h->lmul, h->P.lmul, h->stream);
+}
+
+
+// ---- co-scheduled evaluations (hm_loglik_batch, hm_loglik_multi) ----------
+int max_group(const hm_handle_s* h) {
+    return std::max(std::max(h->rec.max_nsub, h->chol.max_nsub), std::max(h->solve.max_nsub, h->lmul.max_nsub));
+}
+// CTAs an executor needs so that groups partially claimed by waiting CTAs never
+// exhaust it (exec.cu: grid > RQ_NCOOP * (largest group - 1))
+int ctas_needed(const hm_handle_s* h) { return RQ_NCOOP * (max_group(h) - 1) + 1; }
+
+hm_handle_s* clone_handle(const hm_handle_s* p) {
+    std::unique_ptr<hm_handle_s> h(new hm_handle_s());
+    h->device = p->device;
+    h->prm = p->prm;
+    h->poison = p->poison;
+    h->abs_eps = p->abs_eps;
+    h->exec_mode = p->exec_mode;
+    HM_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+    HM_CUDA_TRY(cudaEventCreate(&h->ev[0]));
+    HM_CUDA_TRY(cudaEventCreate(&h->ev[1]));
+    h->T = p->T;
+    h->P = p->P;
+    setup_device(h.get());
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return h.release();
+}
+
+struct Job {
+    hm_handle_s* bound;   // executor that must run it (hm_loglik_multi) or nullptr (any)
+    hm_theta th;
+    const double* Z;
+    double* out;          // k x 3
+};
+
+// One host thread per executor handle, the persistent executors splitting the SMs
+// (each capped at total / S CTAs for the call).  A job's failure stores
+// (-inf, nan, nan) for its columns; the first error is returned.
+int run_jobs(std::vector<hm_handle_s*>& ex, std::vector<Job>& jobs, int zdev, int k) {
+    const int S = (int)ex.size();
+    const int total = exec_grid_rq();
+    std::vector<int> oldcap(S);
+    for (int i = 0; i < S; ++i) {
+        oldcap[i] = ex[i]->exec_grid_cap;
+        ex[i]->exec_grid_cap = S > 1 ? total / S + (i < total % S ? 1 : 0) : oldcap[i];
+        if (S > 1 && ex[i]->exec_grid_cap < ctas_needed(ex[i])) {
+            for (int j = 0; j <= i; ++j) ex[j]->exec_grid_cap = oldcap[j];
+            throw ApiError(HM_ERR_ARG, "co-scheduling " + std::to_string(S) + " evaluations leaves " +
+                                           std::to_string(total / S) + " CTAs per executor, the plan's cooperative "
+                                           "truncations need " + std::to_string(ctas_needed(ex[i])) +
+                                           " (build with a smaller coop_max)");
+        }
+    }
+    std::atomic<int> next{0};
+    std::mutex mu;
+    int first = HM_OK;
+    std::string msg;
+    auto fail = [&](int rc, const std::string& m) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (first == HM_OK) {
+            first = rc;
+            msg = m;
+        }
+    };
+    auto run_one = [&](hm_handle_s* h, const Job& j) {
+        try {
+            do_assemble(h, j.th);
+            do_cholesky(h);
+            do_loglik(h, j.Z, zdev, k, j.out);
+        } catch (...) {
+            const int rc = translate_exception();
+            fail(rc, hm_last_error());
+            for (int c = 0; c < k; ++c) {
+                j.out[3 * c] = -std::numeric_limits<double>::infinity();
+                j.out[3 * c + 1] = j.out[3 * c + 2] = std::numeric_limits<double>::quiet_NaN();
+            }
+        }
+    };
+    auto worker = [&](int i) {
+        hm_handle_s* h = ex[i];
+        if (cudaSetDevice(h->device) != cudaSuccess) {
+            fail(HM_ERR_CUDA, "cudaSetDevice failed in a co-scheduling thread");
+            return;
+        }
+        if (jobs.empty()) return;
+        if (jobs[0].bound) {   // bound jobs: executor i runs the jobs bound to it
+            for (const Job& j : jobs)
+                if (j.bound == h) run_one(h, j);
+            return;
+        }
+        for (int q = next++; q < (int)jobs.size(); q = next++) run_one(h, jobs[q]);
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < S; ++i) th.emplace_back(worker, i);
+    worker(0);
+    for (auto& t : th) t.join();
+    for (int i = 0; i < S; ++i) {
+        ex[i]->exec_grid_cap = oldcap[i];
+        ex[i]->assembled = ex[i]->factored = false;   // state after a batch: assemble again
+    }
+    if (first != HM_OK) set_error(first, msg);
+    return first;
+}
+
 }  // namespace
 
 extern "C" {
@@ -350,6 +495,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (params.coop_max <= 0) params.coop_max = TR_COOP_DEFAULT;
         if (params.coop_max > TR_COOP_MAX) throw ApiError(HM_ERR_ARG, "coop_max <= 32 required");
         if (params.kmax > TR_LMAX - TR_RB) throw ApiError(HM_ERR_ARG, "kmax <= 240 required");
+        if (params.exec_ctas < 0) throw ApiError(HM_ERR_ARG, "exec_ctas >= 0 required");
         check_theta(theta);
         DeviceGuard dg(device);
         h = new hm_handle_s();
@@ -357,6 +503,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         h->prm = params;
         if (const char* pz = std::getenv("HM_POISON_RING")) h->poison = pz[0] == '1';
         h->abs_eps = params.rel_eps == 0;
+        h->exec_grid_cap = params.exec_ctas;
         if (stream) {
             h->stream = (cudaStream_t)stream;
         } else {
@@ -374,37 +521,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         }
         build_tree(hp, n, params.leaf, params.eta, h->T);
         build_plan(h->T, params.kmax, h->P, params.coop_max);
-        vm_set_attr();
-        h->pool.alloc(sizeof(double) * (size_t)std::max<int64_t>(h->P.pool_total, 1));
-        upload(h->pts, h->T.pts, h->stream);
-        upload(h->perm, h->T.perm, h->stream);
-        h->ranks.alloc(sizeof(int) * (h->P.n_slots + 1));
-        HM_CUDA_TRY(cudaMemsetAsync(h->ranks.p, 0, sizeof(int) * (h->P.n_slots + 1), h->stream));
-        h->flags.alloc(sizeof(int) * 4);
-        h->ctr.alloc(sizeof(double) * CTR_N);
-        {
-            size_t mx = 1;
-            for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) mx = std::max(mx, ph->xt.size());
-            h->done.alloc(sizeof(int) * mx);
-            HM_CUDA_TRY(cudaMemsetAsync(h->done.p, 0, sizeof(int) * mx, h->stream));
-            h->counter.alloc(sizeof(int) * 4);
-            h->rq_cnt.alloc(sizeof(int) * mx);
-            h->rq_slot.alloc(sizeof(int) * mx);
-            h->rq_ctl.alloc(sizeof(int) * (2 * RQ_NQ + 2));
-            int nb = 1;
-            for (const Phase* ph : {&h->P.recompress, &h->P.chol, &h->P.solve, &h->P.lmul}) nb = std::max(nb, ph->n_bars);
-            h->bars.alloc(sizeof(int) * nb);
-            exec_grid();
-            exec_grid_rq();
-        }
-        HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
-        h->out.alloc(sizeof(double) * 3 * h->P.zw);
-        upload(h->dgen, h->P.dgen, h->stream);
-        upload(h->aca, h->P.aca, h->stream);
-        upload_phase(h->rec, h->P.recompress, h->stream);
-        upload_phase(h->chol, h->P.chol, h->stream);
-        upload_phase(h->solve, h->P.solve, h->stream);
-        upload_phase(h->lmul, h->P.lmul, h->stream);
+        setup_device(h);
         do_assemble(h, theta);
         *out = h;
         return HM_OK;
@@ -465,25 +582,58 @@ int hm_loglik_batch(hm_handle h, const hm_theta* thetas, int32_t n_theta, const 
         if (!h || !thetas || !Z || !out_host) throw ApiError(HM_ERR_ARG, "null pointer");
         if (k < 1 || n_theta < 0) throw ApiError(HM_ERR_ARG, "k >= 1, n_theta >= 0 required");
         DeviceGuard dg(h->device);
-        int first = HM_OK;
-        for (int i = 0; i < n_theta; ++i) {
-            double* o = out_host + (int64_t)3 * k * i;
-            try {
-                do_assemble(h, thetas[i]);
-                do_cholesky(h);
-                do_loglik(h, Z, z_on_device, k, o);
-            } catch (const ApiError& e) {
-                if (first == HM_OK) first = set_error(e.code, e.what());
-                for (int c = 0; c < k; ++c) {
-                    o[3 * c] = -std::numeric_limits<double>::infinity();
-                    o[3 * c + 1] = o[3 * c + 2] = std::numeric_limits<double>::quiet_NaN();
-                }
-            }
+        for (int i = 0; i < n_theta; ++i) check_theta(thetas[i]);
+        // S co-scheduled executors: the handle + S - 1 siblings on the same tree and plan
+        const int total = exec_grid_rq();
+        int S = h->batch_streams > 0 ? h->batch_streams : 4;
+        S = std::max(1, std::min(S, total / ctas_needed(h)));
+        S = std::min(S, std::max(1, n_theta));
+        try {
+            while ((int)h->subs.size() < S - 1) h->subs.emplace_back(clone_handle(h));
+        } catch (const ApiError& e) {   // out of device memory: co-schedule what exists
+            if (e.code != HM_ERR_OOM) throw;
+            S = 1 + (int)h->subs.size();
         }
-        return first;
+        std::vector<hm_handle_s*> ex{h};
+        for (int i = 0; i < S - 1; ++i) ex.push_back(h->subs[i].get());
+        std::vector<Job> jobs;
+        for (int i = 0; i < n_theta; ++i) jobs.push_back(Job{nullptr, thetas[i], Z, out_host + (int64_t)3 * k * i});
+        return run_jobs(ex, jobs, z_on_device, k);
     } catch (...) {
         return translate_exception();
     }
+}
+
+int hm_loglik_multi(int32_t nh, const hm_handle* hs, const hm_theta* thetas, const double* const* Zs,
+                    int32_t z_on_device, int32_t k, double* out_host) {
+    try {
+        if (nh < 1 || !hs || !thetas || !Zs || !out_host) throw ApiError(HM_ERR_ARG, "null pointer or nh < 1");
+        if (k < 1) throw ApiError(HM_ERR_ARG, "k >= 1 required");
+        std::vector<hm_handle_s*> ex;
+        std::vector<Job> jobs;
+        for (int i = 0; i < nh; ++i) {
+            if (!hs[i] || !Zs[i]) throw ApiError(HM_ERR_ARG, "null handle or data pointer");
+            if (hs[i]->device != hs[0]->device) throw ApiError(HM_ERR_ARG, "all handles must be on one device");
+            for (int j = 0; j < i; ++j)
+                if (hs[j] == hs[i]) throw ApiError(HM_ERR_ARG, "a handle appears twice");
+            check_theta(thetas[i]);
+            ex.push_back(hs[i]);
+            jobs.push_back(Job{hs[i], thetas[i], Zs[i], out_host + (int64_t)3 * k * i});
+        }
+        DeviceGuard dg(hs[0]->device);
+        return run_jobs(ex, jobs, z_on_device, k);
+    } catch (...) {
+        return translate_exception();
+    }
+}
+
+int hm_set_batch_streams(hm_handle h, int32_t streams) {
+    if (!h) return set_error(HM_ERR_ARG, "null handle");
+    if (streams < 0 || streams > 16) return set_error(HM_ERR_ARG, "streams must be in [0, 16]");
+    h->batch_streams = streams;
+    if (streams > 0)
+        while ((int)h->subs.size() > streams - 1) h->subs.pop_back();   // release surplus siblings
+    return HM_OK;
 }
 
 int hm_sample(hm_handle h, const double* xi, int32_t xi_on_device, int32_t k, double* Z, int32_t z_on_device) {
@@ -571,23 +721,28 @@ int hm_stats(hm_handle h, double st[12]) {
     }
 }
 
+static void profile_one(hm_handle_s* h, bool on) {
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    h->profiling = on;
+    h->evlog.clear();
+    // create the event pool up front: creating events while other streams run kernels
+    // serialises co-scheduled handles (measured: 2 streams 2.69 -> 1.46 evals/s)
+    while (h->profiling && h->evpool.size() < 4096) {
+        cudaEvent_t e;
+        HM_CUDA_TRY(cudaEventCreate(&e));
+        h->evpool.push_back(e);
+    }
+    for (auto& x : h->launches) x = 0;
+    HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+}
+
 int hm_profile(hm_handle h, int32_t enable) {
     try {
         if (!h) throw ApiError(HM_ERR_ARG, "null handle");
         DeviceGuard dg(h->device);
-        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
-        h->profiling = enable != 0;
-        h->evlog.clear();
-        // create the event pool up front: creating events while other streams run kernels
-        // serialises co-scheduled handles (measured: 2 streams 2.69 -> 1.46 evals/s)
-        while (h->profiling && h->evpool.size() < 4096) {
-            cudaEvent_t e;
-            HM_CUDA_TRY(cudaEventCreate(&e));
-            h->evpool.push_back(e);
-        }
-        for (auto& x : h->launches) x = 0;
-        HM_CUDA_TRY(cudaMemsetAsync(h->ctr.p, 0, sizeof(double) * CTR_N, h->stream));
-        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        profile_one(h, enable != 0);
+        for (auto& sb : h->subs) profile_one(sb.get(), enable != 0);   // hm_loglik_batch siblings
         return HM_OK;
     } catch (...) {
         return translate_exception();
@@ -709,29 +864,35 @@ int hm_set_exec_grid(hm_handle h, int32_t ctas) {
     return HM_OK;
 }
 
+static void kernel_stats_one(hm_handle_s* h, double out[24]) {
+    HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    double ms[KF_N] = {0, 0, 0, 0, 0, 0};
+    for (auto& e : h->evlog) {
+        float t = 0;
+        HM_CUDA_TRY(cudaEventElapsedTime(&t, h->evpool[e.second], h->evpool[e.second + 1]));
+        ms[e.first] += t;
+    }
+    double c[CTR_N];
+    HM_CUDA_TRY(cudaMemcpy(c, h->ctr.p, sizeof(double) * CTR_N, cudaMemcpyDeviceToHost));
+    const int cmap[KF_N] = {CTR_DGEN, CTR_ACA, CTR_TRUNC, CTR_VM, -1, -1};
+    for (int f = 0; f < KF_N; ++f) {
+        out[4 * f + 0] += (double)h->launches[f];
+        out[4 * f + 1] += ms[f];
+        out[4 * f + 2] += cmap[f] >= 0 ? c[cmap[f]] : 0.0;
+        out[4 * f + 3] += cmap[f] >= 0 ? c[cmap[f] + 1] : 0.0;
+    }
+    // the persistent executor runs the truncation and tile-VM tasks: its work is theirs
+    out[4 * KF_EXEC + 2] += c[CTR_TRUNC] + c[CTR_VM];
+    out[4 * KF_EXEC + 3] += c[CTR_TRUNC + 1] + c[CTR_VM + 1];
+}
+
 int hm_kernel_stats(hm_handle h, double out[24]) {
     try {
         if (!h || !out) throw ApiError(HM_ERR_ARG, "null pointer");
         DeviceGuard dg(h->device);
-        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
-        double ms[KF_N] = {0, 0, 0, 0, 0, 0};
-        for (auto& e : h->evlog) {
-            float t = 0;
-            HM_CUDA_TRY(cudaEventElapsedTime(&t, h->evpool[e.second], h->evpool[e.second + 1]));
-            ms[e.first] += t;
-        }
-        double c[CTR_N];
-        HM_CUDA_TRY(cudaMemcpy(c, h->ctr.p, sizeof(double) * CTR_N, cudaMemcpyDeviceToHost));
-        const int cmap[KF_N] = {CTR_DGEN, CTR_ACA, CTR_TRUNC, CTR_VM, -1, -1};
-        for (int f = 0; f < KF_N; ++f) {
-            out[4 * f + 0] = (double)h->launches[f];
-            out[4 * f + 1] = ms[f];
-            out[4 * f + 2] = cmap[f] >= 0 ? c[cmap[f]] : 0.0;
-            out[4 * f + 3] = cmap[f] >= 0 ? c[cmap[f] + 1] : 0.0;
-        }
-        // the persistent executor runs the truncation and tile-VM tasks: its work is theirs
-        out[4 * KF_EXEC + 2] = c[CTR_TRUNC] + c[CTR_VM];
-        out[4 * KF_EXEC + 3] = c[CTR_TRUNC + 1] + c[CTR_VM + 1];
+        for (int i = 0; i < 24; ++i) out[i] = 0.0;
+        kernel_stats_one(h, out);
+        for (auto& sb : h->subs) kernel_stats_one(sb.get(), out);   // hm_loglik_batch siblings
         return HM_OK;
     } catch (...) {
         return translate_exception();

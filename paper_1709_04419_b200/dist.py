@@ -39,6 +39,8 @@ def gather_results(local: np.ndarray, n_items: int, rank: int, world: int, devic
     buf = np.full((per,) + tail, np.nan)
     buf[: local.shape[0]] = local
     t = torch.from_numpy(buf)
+    if device is None and dist.get_backend() == "nccl":   # NCCL moves device tensors only
+        device = torch.device("cuda", torch.cuda.current_device())
     if device is not None:
         t = t.to(device)
     parts = [torch.empty_like(t) for _ in range(world)]

@@ -98,66 +98,116 @@ def mle_replicate(H, Z, theta0, evals: int = 60, step: float = 0.3):
     return np.exp(x), -fx, len(hist)
 
 
+class _LockstepBatcher:
+    """Runs S Nelder-Mead searches in lockstep: each search (its own host thread)
+    posts its next theta and waits; when every live search has posted, ONE
+    hm_loglik_multi call evaluates them all co-scheduled on the GPU (C-ABI,
+    include/hmlik.h) and hands the results back.  The searches stay in step
+    because each spends exactly the same budget of evaluations."""
+
+    def __init__(self, handles, Zs):
+        import threading
+        self.H, self.Z = handles, Zs
+        self.live = len(handles)
+        self.req = {}
+        self.res = {}
+        self.cv = threading.Condition()
+        self.gen = 0
+
+    def _flush(self):
+        from ._binding import loglik_multi
+        idx = sorted(self.req)
+        out, _ = loglik_multi([self.H[i] for i in idx], [self.req[i] for i in idx], [self.Z[i] for i in idx])
+        for j, i in enumerate(idx):
+            v = out[j, 0, 0]
+            self.res[i] = -float(v) if math.isfinite(v) else math.inf
+        self.req.clear()
+        self.gen += 1
+        self.cv.notify_all()
+
+    def negll(self, i, x):
+        th = tuple(float(v) for v in np.exp(x))
+        with self.cv:
+            self.req[i] = th
+            g = self.gen
+            if len(self.req) == self.live:
+                self._flush()
+            while self.gen == g:
+                self.cv.wait()
+            return self.res.pop(i)
+
+    def done(self):
+        with self.cv:
+            self.live -= 1
+            if self.live > 0 and len(self.req) == self.live:
+                self._flush()
+
+
 def mc_mle(n: int, replicates: int, theta_true, theta0, eps: float = 1e-6, evals: int = 60, leaf: int = 32,
            eta: float = 2.0, rank: int = 0, world: int = 1, device: int = 0, seed: int = 0, gather: bool = True,
-           streams=None, sms: int = 0, kmax: int = 0):
+           streams: int = 1, sms: int = 148, kmax: int = 0):
     """configs[3]: `replicates` independent data sets (n uniform iid locations in
-    [0,1]^2, Z = L~(theta_true) xi drawn by the library's H-sampler at eps/100),
+    [0,1]^2, Z = L~(theta_true) xi drawn by the library's H-sampler at min(eps, 1e-8)),
     each fitted by `evals` Nelder-Mead evaluations.  Replicates are sharded
     round-robin over ranks; returns (replicates x 5): sigma2, ell, nu, loglik, evals.
 
-    streams: optional list of S CUDA stream handles; the rank's replicates are then
-    co-scheduled on the GPU, S at a time (one host thread, stream and handle each,
-    executor capped at sms / S CTAs, cooperative truncations of <= 8 CTAs --
-    hm_set_exec_grid); results are identical to the sequential run."""
+    streams = S > 1: the rank's replicates are fitted S at a time, their searches in
+    lockstep, every round of S likelihood evaluations ONE hm_loglik_multi call
+    (S handles co-scheduled behind the C-ABI, each executor on sms / S CTAs,
+    cooperative truncation groups sized to fit that share); the results equal the
+    one-at-a-time run on the same plan (the CTA cap never changes the arithmetic)."""
     import threading
 
     from ._binding import HMatrix
     from synthetic import standard_normal, uniform_iid
 
     mine = list(shard_indices(replicates, rank, world))
-    S = len(streams) if streams else 1
+    S = max(1, int(streams))
+    cap = sms // S if S > 1 else 0
+    # deadlock bound of the ready-queue executor: 4 * (coop - 1) < CTAs per executor
+    coop = 16 if S == 1 else max(1, min(8, (cap - 1) // 4 + 1))
+    kw = dict(leaf=leaf, eta=eta, device=device, kmax=kmax, coop_max=coop, exec_ctas=cap)
     res = {}
 
-    def fit(r, stream, cap):
-        kw = dict(leaf=leaf, eta=eta, device=device, kmax=kmax)
-        if stream is not None:
-            kw.update(stream=stream, coop_max=8)
+    def data(r):
         pts = uniform_iid(n, seed + 1000 * int(r))
         Hs = HMatrix(pts, theta_true, eps=min(eps, 1e-8), **kw)
-        if cap:
-            Hs.set_exec_grid(cap)
         Hs.cholesky()
         Z = Hs.sample(standard_normal(n, 1, seed + 1000 * int(r) + 1))[:, 0]
         Hs.close()
-        H = HMatrix(pts, theta0, eps=eps, **kw)
-        if cap:
-            H.set_exec_grid(cap)
-        th, ll, ne = mle_replicate(H, Z, theta0, evals=evals)
-        H.close()
-        res[r] = [th[0], th[1], th[2], ll, ne]
+        return pts, Z
 
-    if S <= 1:
-        for r in mine:
-            fit(r, None, 0)
-    else:
-        caps = [sms // S + (1 if i < sms % S else 0) for i in range(S)]
-        errs = []
+    for g0 in range(0, len(mine), S):
+        group = mine[g0:g0 + S]
+        sets = [data(r) for r in group]
+        Hs = [HMatrix(p, theta0, eps=eps, **kw) for p, _ in sets]
+        if len(group) == 1:
+            th, ll, ne = mle_replicate(Hs[0], sets[0][1], theta0, evals=evals)
+            res[group[0]] = [th[0], th[1], th[2], ll, ne]
+        else:
+            B = _LockstepBatcher(Hs, [Z for _, Z in sets])
+            errs = []
 
-        def worker(i):
-            try:
-                for r in mine[i::S]:
-                    fit(r, streams[i], caps[i])
-            except Exception as e:  # surfaced after the join
-                errs.append(e)
+            def search(i, r):
+                try:
+                    x, fx, hist = nelder_mead(lambda x: B.negll(i, x), np.log(np.asarray(theta0, dtype=np.float64)),
+                                              0.3, evals)
+                    th = np.exp(x)
+                    res[r] = [th[0], th[1], th[2], -fx, len(hist)]
+                except Exception as e:  # surfaced after the join
+                    errs.append(e)
+                finally:
+                    B.done()
 
-        th = [threading.Thread(target=worker, args=(i,)) for i in range(S)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        if errs:
-            raise errs[0]
+            ts = [threading.Thread(target=search, args=(i, r)) for i, r in enumerate(group)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            if errs:
+                raise errs[0]
+        for H in Hs:
+            H.close()
     out = [res[r] for r in mine]
     local = np.asarray(out, dtype=np.float64).reshape(-1, 5)
     if world > 1 and gather:

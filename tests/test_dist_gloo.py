@@ -82,3 +82,47 @@ def test_sharded_evaluation_world2(n_theta):
         np.testing.assert_allclose(out[:, 0, 0], thetas[:, 0] + 10 * thetas[:, 1] + 100 * thetas[:, 2])
         np.testing.assert_array_equal(out[:, 1, 1], owners)
 
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's rank logic on CPU: each rank's theta slice (rank_thetas) and the
+    gather of the per-evaluation (loglik, logdet, quad) triples after the timed region."""
+    import sys
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_1709_04419_b200.dist import gather_results
+    w = bench.WORKLOADS["n64k"]
+    S, steps = 4, 3
+    mine = bench.rank_thetas(w, steps, S, rank, world)
+    res = np.array([[th[1], th[2], float(rank)] for th in mine])   # stands in for loglik_batch output
+    allres = gather_results(res, len(res) * world, rank, world)
+    q.put((rank, mine, allres))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_rank_logic_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    full = bench.theta_schedule(bench.WORKLOADS["n64k"], 3 * 2 * 4)
+    got = sorted(tuple(th) for r in res for th in r[1])
+    assert got == sorted(map(tuple, full)) and len(res[0][1]) == len(res[1][1]) == 12   # disjoint, complete
+    np.testing.assert_array_equal(res[0][2], res[1][2])                               # same gathered table
+    assert sorted(res[0][2][:, 2].tolist()) == [0.0] * 12 + [1.0] * 12                 # every rank's rows

@@ -97,5 +97,34 @@ def test_dense_device_pointers(hm):
 def test_dense_errors(hm):
     with pytest.raises(hm.HMError):
         hm.dense_loglik(uniform_iid(10, 0), (1.0, -0.1, 0.5), np.zeros(10))
-    with pytest.raises(hm.HMError):
-        hm.dense_loglik(uniform_iid(16385, 0), (1.0, 0.1, 0.5), np.zeros(16385))
+    with pytest.raises(hm.HMError) as e:
+        hm.dense_loglik(uniform_iid(131073, 0), (1.0, 0.1, 0.5), np.zeros(131073))
+    assert e.value.code == -7
+    with pytest.raises(ValueError):
+        hm.dense_loglik(uniform_iid(10, 0), (1.0, 0.1, 0.5), np.zeros(11))
+
+
+def test_dense_65536_exponential_line_closed_form(hm):
+    """The dense check path at configs[2]'s size (n = 65,536, the reference of the
+    full-size mesh tests): exponential covariance on an equispaced line has
+    log det C = n log sigma^2 + (n-1) log(1 - rho^2) and a tridiagonal inverse
+    (the closed forms pinned in test_oracle_dense.py), Z drawn by the AR(1)
+    recursion.  North-star bar 1e-10 relative."""
+    import math
+    n, sigma2, ell = 65536, 1.3, 0.1
+    pts = np.stack([(np.arange(n) + 0.5) / n, np.zeros(n)], axis=1)
+    rho = math.exp(-1.0 / (n * ell))
+    xi = standard_normal(n, 1, seed=40)[:, 0]
+    z = np.empty(n)
+    z[0] = math.sqrt(sigma2) * xi[0]
+    s = math.sqrt(sigma2 * (1 - rho * rho))
+    for i in range(1, n):
+        z[i] = rho * z[i - 1] + s * xi[i]
+    logdet = n * math.log(sigma2) + (n - 1) * math.log1p(-rho * rho)
+    quad = ((1 + rho * rho) * np.sum(z * z) - rho * rho * (z[0] ** 2 + z[-1] ** 2)
+            - 2 * rho * np.sum(z[:-1] * z[1:])) / (sigma2 * (1 - rho * rho))
+    ll = -0.5 * n * math.log(2 * math.pi) - 0.5 * logdet - 0.5 * quad
+    got = hm.dense_loglik(pts, (sigma2, ell, 0.5), z)[0]
+    assert abs(got[0] - ll) <= 1e-10 * abs(ll)
+    assert abs(got[1] - logdet) <= 1e-10 * abs(logdet)
+    assert abs(got[2] - quad) <= 1e-10 * abs(ll)

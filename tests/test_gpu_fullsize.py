@@ -60,6 +60,40 @@ def test_exponential_line_closed_form(hm, n, eps, tol):
     assert abs(got[2] - q) <= tol * abs(ll)
 
 
+@pytest.fixture(scope="module")
+def mesh64k(hm):
+    """configs[2] locations, Z drawn by the H sampler at eps = 1e-10 for each nu (an
+    input shared by both sides), and the GPU dense fp64 reference at n = 65,536
+    (34 GB; pinned by the closed form in test_gpu_dense.py)."""
+    pts = perturbed_mesh(256, 0.4, 2)
+    ref = {}
+    for nu in (0.5, 1.0):
+        th = (1.0, 0.1, nu)
+        Hs = hm.HMatrix(pts, th, eps=1e-10, leaf=64, eta=2.0)
+        Hs.cholesky()
+        Z = Hs.sample(standard_normal(len(pts), 1, seed=42))[:, 0]
+        Hs.close()
+        ref[nu] = (Z, hm.dense_loglik(pts, th, Z)[0])
+    return pts, ref
+
+
+@pytest.mark.parametrize("nu", [0.5, 1.0])
+@pytest.mark.parametrize("eps,tol", [(1e-8, 1e-6), (1e-7, 1e-6), (1e-5, 1e-4)])
+def test_mesh_64k_vs_dense(hm, mesh64k, nu, eps, tol):
+    """configs[2] at full size (n = 65,536 jittered mesh, Eq. 3; leaf 64, kmax 64 as
+    bench.py runs it) against the exact likelihood: nu = 0.5 (exponential) and
+    nu = 1.0 (the general-nu Bessel path).  Measured (r02): 1.1e-9 / 6.5e-9 / 2.0e-7
+    (nu = 0.5) and 1.5e-9 / 4.2e-9 / 1.0e-6 (nu = 1.0) at eps = 1e-8 / 1e-7 / 1e-5."""
+    pts, ref = mesh64k
+    Z, d = ref[nu]
+    H = hm.HMatrix(pts, (1.0, 0.1, nu), eps=eps, leaf=64, eta=2.0, kmax=64)
+    H.cholesky()
+    g = H.loglik(Z)[0]
+    assert abs(g[0] - d[0]) <= tol * abs(d[0])
+    assert abs(g[1] - d[1]) <= tol * abs(d[0])
+    assert abs(g[2] - d[2]) <= tol * abs(d[0])
+
+
 def test_mesh_64k_sampler_roundtrip(hm):
     """configs[2] (n = 65,536 jittered mesh, leaf 64, eps = 1e-7): the factor's own
     sampler and solve are inverse to each other -- quad(L~ xi) = ||xi||^2 -- and a

@@ -251,3 +251,64 @@ def test_plan_parameter_validation(hm):
     with pytest.raises(hm.HMError) as ei:
         hm.HMatrix(pts, (1.0, 0.1, 0.5), eps=1e-6, leaf=32, kmax=300)
     assert ei.value.code == -1
+
+
+def test_loglik_batch_coscheduled_in_c(hm):
+    """hm_loglik_batch co-schedules its thetas behind the C-ABI (S executors = the
+    handle + S - 1 siblings, one host thread each, SMs split): bit-identical to one
+    evaluation at a time, for S = 4 (coop_max 8), S = 2, the automatic choice and S = 1,
+    with more thetas than executors."""
+    pts = uniform_iid(16384, 5)
+    Z = standard_normal(16384, 2, 6)
+    ths = [(1.0, 0.05, 0.5), (1.3, 0.08, 1.0), (0.9, 0.03, 0.7), (1.1, 0.06, 1.4), (1.0, 0.04, 0.9),
+           (1.2, 0.07, 0.6)]
+    H = hm.HMatrix(pts, ths[0], eps=1e-7, leaf=32, coop_max=8)
+    ref = []
+    for th in ths:
+        H.assemble(th)
+        H.cholesky()
+        ref.append(H.loglik(Z))
+    ref = np.stack(ref)
+    for S in (4, 2, 0, 1):
+        H.set_batch_streams(S)
+        out, rc = H.loglik_batch(ths, Z)
+        assert rc == 0
+        assert np.array_equal(out, ref), S
+    with pytest.raises(hm.HMError) as ei:   # the handle holds no factor after a batch
+        H.loglik(Z)
+    assert ei.value.code == -6
+    more = ths + ths[:3]
+    H.set_batch_streams(4)
+    out, rc = H.loglik_batch(np.array(more), Z)
+    assert rc == 0 and np.array_equal(out[6:], ref[:3]) and np.array_equal(out[:6], ref)
+    with pytest.raises(hm.HMError):
+        H.set_batch_streams(17)
+    H.close()
+
+
+def test_loglik_multi_different_locations(hm):
+    """hm_loglik_multi: handles on different location sets (Monte-Carlo replicates,
+    PAPER.md sec. 4) evaluated concurrently, each on its own data, equal to the
+    same evaluations one at a time; too many handles for the plans' cooperative
+    groups is refused."""
+    Hs, Zs, ths, ref = [], [], [], []
+    for r in range(3):
+        pts = uniform_iid(4096, 50 + r)
+        th = (1.0, 0.05 + 0.01 * r, 0.5 + 0.2 * r)
+        H = hm.HMatrix(pts, th, eps=1e-7, leaf=32, coop_max=8)
+        H.cholesky()
+        Z = standard_normal(4096, 1, 60 + r)
+        ref.append(H.loglik(Z))
+        Hs.append(H)
+        Zs.append(Z)
+        ths.append(th)
+    out, rc = hm.loglik_multi(Hs, ths, Zs)
+    assert rc == 0 and np.array_equal(out, np.stack(ref))
+    import torch
+    Zd = [torch.tensor(Z[:, 0], device="cuda") for Z in Zs]
+    out2, rc = hm.loglik_multi(Hs, ths, Zd)
+    assert rc == 0 and np.array_equal(out2, out)
+    H16 = [hm.HMatrix(uniform_iid(16384, 70 + r), ths[0], eps=1e-7, leaf=32, coop_max=32) for r in range(4)]
+    with pytest.raises(hm.HMError):
+        _, rc = hm.loglik_multi(H16, [ths[0]] * 4, [Zs[0]] * 4)
+        hm._binding.check(rc)
