@@ -1,5 +1,9 @@
 // Host setup of the theta-dependent constants of the device Matern kernel
-// (Eq. 2, l.183-188).  See matern.cuh for the device algorithm.
+// (Eq. 2, l.183-188).  See matern.cuh for the device algorithm and its
+// sources (Temme 1975; Thompson & Barnett 1987): the order split nu = n + mu and
+// Temme's Gamma-function combinations
+//   G1(mu) = (1/Gamma(1-mu) - 1/Gamma(1+mu)) / (2 mu),  G2(mu) = (1/Gamma(1-mu) + 1/Gamma(1+mu)) / 2,
+// evaluated from the Taylor series of 1/Gamma (accurate also as mu -> 0).
 #include <cmath>
 
 #include "common.h"

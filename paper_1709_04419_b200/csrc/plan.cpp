@@ -265,6 +265,21 @@ struct Builder {
         for (auto& v : pre) v.clear();
     }
     // wave after which the data in resources `rs` (a product's source) is available
+    // earliest wave the product H(Yb) x V could be computed in (wave rule of arena_take)
+    int32_t wnat_of(int32_t Yb, const Thin& V) const {
+        return wnat_mode ? std::max(avail_block(Yb), avail_wave(V)) : avail_wave(V);
+    }
+    int wnat_mode = 1;
+    // wave after which every block of the subtree of b (the other factor of a product) is final
+    int32_t avail_block(int32_t b) const {
+        const BStore& st = P.bs[b];
+        if (st.kind == ST_DENSE) return lw_wave[st.d_res] + 1;
+        if (st.kind == ST_LR) return std::max(avail_wave(thin_U(b)), avail_wave(thin_V(b)));
+        int32_t w = 0;
+        for (int i = 0; i < 4; ++i)
+            if (B(b).child[i] >= 0) w = std::max(w, avail_block(B(b).child[i]));
+        return w;
+    }
     int32_t avail_wave(const Thin& M) const {
         int32_t w = 0;
         for (int32_t i = 0; i < P.leaf_count[M.cluster]; ++i) w = std::max(w, lw_wave[M.res0 + i] + 1);
@@ -785,13 +800,13 @@ struct Builder {
                         pend[c[0]].prods.push_back({B(X).child[c[1] + 2 * j], B(Y).child[c[2] + 2 * j]});
             } else if (kx == ST_LR) {
                 cur_site = 1;
-                Thin Tm = new_thin(bb.s, P.bs[X].cap, P.bs[X].rslot, avail_wave(thin_V(X)));
+                Thin Tm = new_thin(bb.s, P.bs[X].cap, P.bs[X].rslot, wnat_of(Y, thin_V(X)));
                 hxt(Y, thin_V(X), Tm, 1.0, false);
                 pd.pieces.push_back(LPiece{thin_U(X), Tm, -1.0});
                 piece_ref(pd.pieces.back(), +1);
             } else if (ky == ST_LR) {
                 cur_site = 1;
-                Thin Tm = new_thin(bb.t, P.bs[Y].cap, P.bs[Y].rslot, avail_wave(thin_V(Y)));
+                Thin Tm = new_thin(bb.t, P.bs[Y].cap, P.bs[Y].rslot, wnat_of(X, thin_V(Y)));
                 hxt(X, thin_V(Y), Tm, 1.0, false);
                 pd.pieces.push_back(LPiece{Tm, thin_U(Y), -1.0});
                 piece_ref(pd.pieces.back(), +1);
@@ -886,13 +901,13 @@ struct Builder {
         const int32_t kx = P.bs[X].kind, ky = P.bs[Y].kind;
         if (kx == ST_LR) {
             cur_site = 2;
-            Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot, avail_wave(thin_V(X)));
+            Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot, wnat_of(Y, thin_V(X)));
             hxt(Y, thin_V(X), Tm, 1.0, false);
             out.push_back(tpiece(thin_U(X), Tm, row0, col0, -1.0, reads));
             temps.push_back(Tm);
         } else if (ky == ST_LR) {
             cur_site = 2;
-            Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot, avail_wave(thin_V(Y)));
+            Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot, wnat_of(X, thin_V(Y)));
             hxt(X, thin_V(Y), Tm, 1.0, false);
             out.push_back(tpiece(Tm, thin_U(Y), row0, col0, -1.0, reads));
             temps.push_back(Tm);
@@ -1300,6 +1315,7 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
     // temporaries of every phase live in one arena above the permanent storage
     bld.arena_base = bld.bump;
     if (const char* am = std::getenv("HM_ARENA_MODE")) bld.arena_mode = std::atoi(am);
+    if (const char* wm = std::getenv("HM_WNAT_MODE")) bld.wnat_mode = std::atoi(wm);
     bld.arena_budget = arena_budget;
     if (const char* ab = std::getenv("HM_ARENA_BUDGET")) bld.arena_budget = std::atoll(ab);
     // recompression of every ACA block: a truncation with the block itself as the only piece

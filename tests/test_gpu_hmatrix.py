@@ -309,6 +309,7 @@ def test_loglik_multi_different_locations(hm):
     out2, rc = hm.loglik_multi(Hs, ths, Zd)
     assert rc == 0 and np.array_equal(out2, out)
     H16 = [hm.HMatrix(uniform_iid(16384, 70 + r), ths[0], eps=1e-7, leaf=32, coop_max=32) for r in range(4)]
+    Z16 = standard_normal(16384, 1, 80)
     with pytest.raises(hm.HMError):
-        _, rc = hm.loglik_multi(H16, [ths[0]] * 4, [Zs[0]] * 4)
+        _, rc = hm.loglik_multi(H16, [ths[0]] * 4, [Z16] * 4)
         hm._binding.check(rc)
