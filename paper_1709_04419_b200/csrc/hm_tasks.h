@@ -89,6 +89,9 @@ struct TTask {
     int32_t wmax;             // largest static piece width
     int32_t nsub;             // CTAs cooperating on this truncation (persistent executor)
     int32_t bar;              // index of its group barrier counter
+    double eps_scale;         // this truncation's share of the block accuracy (1 = all of it;
+                              // a split truncation gives its partial merge and its final step
+                              // shares summing to 1, so the block stays within eps)
 };
 
 // k_trunc algorithm selection and workspace (trunc.cuh; planner sizes the workspace)

@@ -228,8 +228,8 @@ int max_rank(hm_handle_s* h) {
                                 h->stream));
     HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     int mx = 0;
-    for (int i = 0; i < h->P.n_slots; ++i)
-        if (i != h->P.z_slot) mx = std::max(mx, h->h_ranks[i]);   // z_slot: RHS width, not a rank
+    for (int i = 0; i < h->P.n_block_slots; ++i)   // blocks only: z_slot is the RHS width, later
+        if (i != h->P.z_slot) mx = std::max(mx, h->h_ranks[i]);   // slots hold split truncations' partial sums
     return mx;
 }
 
@@ -336,6 +336,17 @@ void do_loglik(hm_handle_s* h, const double* Z, int zdev, int k, double* out_hos
     HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     std::memcpy(out_host, h->pin_out, sizeof(double) * 3 * k);
     h->ms[2] = elapsed(h);
+}
+
+// Device bytes of a plan's task lists and ready-queue schedules (setup_device uploads).
+double plan_device_bytes(const Plan& P) {
+    double b = 0.0;
+    for (const Phase* ph : {&P.recompress, &P.chol, &P.solve, &P.lmul})
+        b += (double)ph->ins.size() * sizeof(VIns) + (double)ph->vt.size() * sizeof(VTask) +
+             (double)ph->tt.size() * sizeof(TTask) + (double)ph->tp.size() * sizeof(TPiece) +
+             (double)ph->terms.size() * sizeof(VTerm) + 3.0 * (double)ph->xt.size() * sizeof(XTask) +
+             3.0 * (double)ph->xdeps.size() * sizeof(int32_t) + 16.0 * (double)ph->xt.size();
+    return b + 8.0 * ((double)P.dgen.size() + (double)P.aca.size()) * 4.0;
 }
 
 // Device side of a handle whose tree and plan are built: pool, task lists, schedules.
@@ -521,6 +532,22 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         }
         build_tree(hp, n, params.leaf, params.eta, h->T);
         build_plan(h->T, params.kmax, h->P, params.coop_max);
+        {
+            // Device memory: if the pool (with the temporaries' arena planned for
+            // parallelism) and the task lists do not fit, plan again with an arena
+            // budget -- memory is then recycled even where that lengthens the
+            // critical path (plan.h build_plan).
+            size_t fr = 0, tot = 0;
+            HM_CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+            const double avail = 0.92 * (double)fr - plan_device_bytes(h->P);
+            if (8.0 * (double)h->P.pool_total > avail) {
+                const double budget = avail / 8.0 - (double)(h->P.pool_total - h->P.arena_size);
+                if (budget < (double)(int64_t(1) << 24))
+                    throw ApiError(HM_ERR_OOM, "H-matrix storage does not fit in device memory (" +
+                                                   std::to_string(8e-9 * h->P.pool_total) + " GB needed)");
+                build_plan(h->T, params.kmax, h->P, params.coop_max, (int64_t)budget);
+            }
+        }
         setup_device(h);
         do_assemble(h, theta);
         *out = h;

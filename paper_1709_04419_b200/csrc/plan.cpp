@@ -897,22 +897,26 @@ struct Builder {
 
     // evaluate product X Y^T into truncation pieces placed at (row0, col0) of the target
     void eval_pieces(int32_t X, int32_t Y, int32_t row0, int32_t col0, std::vector<TPiece>& out,
-                     std::vector<int32_t>& reads, std::vector<Thin>& temps) {
+                     std::vector<std::vector<int32_t>>& pres, std::vector<Thin>& temps) {
+        std::vector<int32_t> reads;
         const int32_t kx = P.bs[X].kind, ky = P.bs[Y].kind;
         if (kx == ST_LR) {
             cur_site = 2;
             Thin Tm = new_thin(B(Y).t, P.bs[X].cap, P.bs[X].rslot, wnat_of(Y, thin_V(X)));
             hxt(Y, thin_V(X), Tm, 1.0, false);
             out.push_back(tpiece(thin_U(X), Tm, row0, col0, -1.0, reads));
+            pres.push_back(std::move(reads));
             temps.push_back(Tm);
         } else if (ky == ST_LR) {
             cur_site = 2;
             Thin Tm = new_thin(B(X).t, P.bs[Y].cap, P.bs[Y].rslot, wnat_of(X, thin_V(Y)));
             hxt(X, thin_V(Y), Tm, 1.0, false);
             out.push_back(tpiece(Tm, thin_U(Y), row0, col0, -1.0, reads));
+            pres.push_back(std::move(reads));
             temps.push_back(Tm);
         } else if (kx == ST_DENSE && ky == ST_DENSE) {
             out.push_back(tpiece(thin_D(X), thin_D(Y), row0, col0, -1.0, reads));
+            pres.push_back(std::move(reads));
         } else if (kx == ST_SUB && ky == ST_SUB) {
             const Cluster& rx = C(B(X).t);
             const Cluster& ry = C(B(Y).t);
@@ -921,7 +925,7 @@ struct Builder {
                     for (int j = 0; j < 2; ++j) {
                         const int32_t cx = B(X).child[i + 2 * j], cy = B(Y).child[k + 2 * j];
                         eval_pieces(cx, cy, row0 + (int32_t)(C(B(cx).t).lo - rx.lo),
-                                    col0 + (int32_t)(C(B(cy).t).lo - ry.lo), out, reads, temps);
+                                    col0 + (int32_t)(C(B(cy).t).lo - ry.lo), out, pres, temps);
                     }
         } else {
             throw std::logic_error("eval_pieces: mixed dense/subdivided factors");
@@ -940,20 +944,50 @@ struct Builder {
         return p;
     }
 
-    // low-rank target: gather own + pending and re-truncate once
+    // Where a truncation writes: the block's own factors or a temporary partial sum.
+    struct TruncTarget {
+        int64_t u_off, v_off;
+        int32_t m, q, cap, rslot;
+    };
+    TruncTarget target_of(int32_t b) const {
+        const BStore& s = P.bs[b];
+        return TruncTarget{s.u_off, s.v_off, s.m, s.p, s.cap, s.rslot};
+    }
+    int32_t ready_wave(const std::vector<int32_t>& res) const {
+        int32_t w = 0;
+        for (int32_t r : res) w = std::max(w, lw_wave[r] + 1);
+        return w;
+    }
+
+    // low-rank target: gather own + pending and re-truncate once.  A wide sum whose
+    // pieces become available at different times is truncated in two steps (split_trunc):
+    // the early pieces (and the block's own factors) are merged into a temporary low-rank
+    // partial sum as soon as they exist, so the step that waits for the last pieces
+    // only handles that partial sum plus those pieces -- a much narrower stack on the
+    // Cholesky's critical path.
     void flush_lr(int32_t b, bool force) {
         Pend pd = std::move(pend[b]);
         pend[b] = Pend();
         if (!force && pd.prods.empty() && pd.pieces.empty()) return;
         std::vector<TPiece> pcs;
-        std::vector<int32_t> reads, writes;
+        std::vector<std::vector<int32_t>> pres;
+        std::vector<int32_t> writes;
         std::vector<Thin> temps;
-        pcs.push_back(tpiece(thin_U(b), thin_V(b), 0, 0, 1.0, reads));
-        for (auto& pc : pd.pieces) pcs.push_back(tpiece(pc.U, pc.V, 0, 0, pc.alpha, reads));
-        for (auto& pr : pd.prods) eval_pieces(pr.first, pr.second, 0, 0, pcs, reads, temps);
+        auto add = [&](const Thin& U, const Thin& V, double alpha) {
+            std::vector<int32_t> r;
+            pcs.push_back(tpiece(U, V, 0, 0, alpha, r));
+            pres.push_back(std::move(r));
+        };
+        add(thin_U(b), thin_V(b), 1.0);
+        for (auto& pc : pd.pieces) add(pc.U, pc.V, pc.alpha);
+        for (auto& pr : pd.prods) eval_pieces(pr.first, pr.second, 0, 0, pcs, pres, temps);
         thin_res(thin_U(b), writes);
         thin_res(thin_V(b), writes);
-        emit_trunc(b, pcs, reads, writes);
+        if (!split_trunc(b, pcs, pres, writes)) {
+            std::vector<int32_t> reads;
+            for (auto& r : pres) reads.insert(reads.end(), r.begin(), r.end());
+            emit_trunc(target_of(b), pcs, reads, writes, 1.0);
+        }
         for (auto& pc : pd.pieces) piece_ref(pc, -1);
         for (auto& t : temps) {
             tmp_ref(t, +1);
@@ -961,17 +995,77 @@ struct Builder {
         }
     }
 
-    void emit_trunc(int32_t b, const std::vector<TPiece>& pcs, std::vector<int32_t>& reads,
-                    std::vector<int32_t>& writes) {
+    bool split_trunc(int32_t b, const std::vector<TPiece>& pcs, const std::vector<std::vector<int32_t>>& pres,
+                     std::vector<int32_t>& writes) {
         const BStore& s = P.bs[b];
+        const int32_t n = (int32_t)pcs.size();
+        int32_t ktot = 0;
+        for (auto& p : pcs) ktot += p.w.stat;
+        if (!split_enabled || n < 4 || ktot <= 4 * s.cap || trunc_exact_path(s.m, s.p, ktot)) return false;
+        std::vector<int32_t> wv(n), order;
+        for (int32_t i = 0; i < n; ++i) wv[i] = ready_wave(pres[i]);
+        for (int32_t i = 1; i < n; ++i) order.push_back(i);   // the block's own factors are early by nature
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return wv[a] > wv[c]; });
+        std::vector<char> late(n, 0);
+        int32_t klate = 0;
+        for (int32_t i : order) {
+            if (klate > 0 && klate + pcs[i].w.stat > 2 * s.cap) break;
+            late[i] = 1;
+            klate += pcs[i].w.stat;
+        }
+        int32_t kearly = ktot - klate, wearly = 0, wlate = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            if (late[i]) wlate = std::max(wlate, wv[i]);
+            else wearly = std::max(wearly, wv[i]);
+        }
+        if (kearly <= 2 * s.cap || wearly >= wlate) return false;   // nothing to hide
+        // partial sum of the early pieces into a temporary (arena) low-rank pair, rank slot of its own
+        const int32_t cap_t = std::min(std::min(s.m, s.p), std::min(2 * s.cap, TR_LMAX - TR_RB));
+        const int32_t slot_t = P.n_slots++;
+        Thin Ut = new_thin(B(b).t, cap_t, slot_t, wearly);
+        Thin Vt = new_thin(B(b).s, cap_t, slot_t, wearly);
+        tmp_ref(Ut, +1);
+        tmp_ref(Vt, +1);
+        std::vector<TPiece> pe;
+        std::vector<int32_t> re, we;
+        for (int32_t i = 0; i < n; ++i)
+            if (!late[i]) {
+                pe.push_back(pcs[i]);
+                re.insert(re.end(), pres[i].begin(), pres[i].end());
+            }
+        thin_res(Ut, we);
+        thin_res(Vt, we);
+        emit_trunc(TruncTarget{Ut.off, Vt.off, s.m, s.p, cap_t, slot_t}, pe, re, we, TRUNC_SPLIT_SHARE);
+        // final step: partial sum + the late pieces -> the block
+        std::vector<TPiece> pf;
+        std::vector<int32_t> rf;
+        pf.push_back(tpiece(Ut, Vt, 0, 0, 1.0, rf));
+        for (int32_t i = 0; i < n; ++i)
+            if (late[i]) {
+                pf.push_back(pcs[i]);
+                rf.insert(rf.end(), pres[i].begin(), pres[i].end());
+            }
+        emit_trunc(target_of(b), pf, rf, writes, 1.0 - TRUNC_SPLIT_SHARE);
+        tmp_ref(Ut, -1);
+        tmp_ref(Vt, -1);
+        ++n_split;
+        return true;
+    }
+    static constexpr double TRUNC_SPLIT_SHARE = 0.25;   // accuracy share of the partial merge
+    bool split_enabled = true;
+    int64_t n_split = 0;
+
+    void emit_trunc(const TruncTarget& tg, const std::vector<TPiece>& pcs, std::vector<int32_t>& reads,
+                    std::vector<int32_t>& writes, double eps_scale) {
         std::sort(reads.begin(), reads.end());
         reads.erase(std::unique(reads.begin(), reads.end()), reads.end());
-        int32_t kt0 = 0, wmax0 = 0;
+        int32_t kt = 0, wmax = 0;
         for (auto& p : pcs) {
-            kt0 += p.w.stat;
-            wmax0 = std::max(wmax0, p.w.stat);
+            kt += p.w.stat;
+            wmax = std::max(wmax, p.w.stat);
         }
-        const int64_t wsz = trunc_ws_size(s.m, s.p, s.cap, kt0, trunc_nsub(s.m, s.p, kt0, coop_max));
+        const int32_t nsub = trunc_nsub(tg.m, tg.q, kt, coop_max);
+        const int64_t wsz = trunc_ws_size(tg.m, tg.q, tg.cap, kt, nsub);
         const int64_t nch = (wsz + ring_chunk - 1) / ring_chunk;
         if (4 * nch > ring_nchunks) grow_ring(4 * nch);   // keep >= 4 workspaces of this size in flight
         if (ring_ptr + nch > ring_nchunks) ring_ptr = 0;
@@ -981,21 +1075,17 @@ struct Builder {
         std::vector<int32_t> deps;
         int32_t w = wave_of(reads, writes, deps);
         TTask t{};
-        t.u_out = s.u_off; t.v_out = s.v_off;
-        t.m = s.m; t.q = s.p; t.cap = s.cap; t.rslot = s.rslot;
+        t.u_out = tg.u_off; t.v_out = tg.v_off;
+        t.m = tg.m; t.q = tg.q; t.cap = tg.cap; t.rslot = tg.rslot;
         t.piece_begin = (int32_t)ph->tp.size();
         t.piece_count = (int32_t)pcs.size();
-        int32_t kt = 0, wmax = 0;
-        for (auto& p : pcs) {
-            kt += p.w.stat;
-            wmax = std::max(wmax, p.w.stat);
-        }
         t.kmax_tot = kt;
         t.wmax = wmax;
         t.ws_size = wsz;
         t.ws = ws_off;
+        t.eps_scale = eps_scale;
         if ((int32_t)pcs.size() > TR_PMAX) throw std::logic_error("truncation with more than TR_PMAX pieces");
-        t.nsub = trunc_nsub(s.m, s.p, kt, coop_max);
+        t.nsub = nsub;
         t.bar = t.nsub > 1 ? ph->n_bars++ : 0;
         ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
         xraw.push_back({w, 1, (int32_t)traw.size(), std::move(deps)});
@@ -1264,6 +1354,7 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
     P.zw = 64;
     P.z_off = bld.alloc((int64_t)T.n * P.zw);
     P.z_slot = P.n_slots++;
+    P.n_block_slots = P.n_slots;
     const int32_t z_res0 = bld.new_res(P.n_leaves);
     P.pool_blocks = bld.bump;
     // temporary 64 x 64 tiles for split dense updates (see apply_dense_pending)
@@ -1316,6 +1407,7 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
     bld.arena_base = bld.bump;
     if (const char* am = std::getenv("HM_ARENA_MODE")) bld.arena_mode = std::atoi(am);
     if (const char* wm = std::getenv("HM_WNAT_MODE")) bld.wnat_mode = std::atoi(wm);
+    if (const char* sp = std::getenv("HM_TRUNC_SPLIT")) bld.split_enabled = std::atoi(sp) != 0;
     bld.arena_budget = arena_budget;
     if (const char* ab = std::getenv("HM_ARENA_BUDGET")) bld.arena_budget = std::atoll(ab);
     // recompression of every ACA block: a truncation with the block itself as the only piece
@@ -1341,6 +1433,7 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
     bld.end_phase();
     for (const auto& a : bld.tmps)
         if (a.refs != 0) throw std::logic_error("planner: live temporary at the end of planning");
+    P.n_split = bld.n_split;
     P.arena_off = bld.arena_base;
     P.arena_size = bld.arena_top;
     bld.bump = bld.arena_base + bld.arena_top;

@@ -89,6 +89,8 @@ struct Plan {
     Phase solve;                       // v <- L~^{-1} z  on the z buffer
     Phase lmul;                        // z <- L~ z       (sampler)
     int64_t n_tasks_chol = 0;
+    int64_t n_split = 0;               // Cholesky truncations split into partial merge + final step
+    int32_t n_block_slots = 0;         // rank slots [0, n_block_slots) belong to blocks (+ z_slot)
     std::string summary() const;
 };
 

@@ -984,6 +984,7 @@ __device__ __forceinline__ void trunc_run(const TTask& t, const TPiece* __restri
                                           int* bar = nullptr, unsigned long long* stt = nullptr) {
     int K = 0;
     for (int p = 0; p < t.piece_count; ++p) K += dim_eval(pieces[t.piece_begin + p].w, ranks);
+    eps *= t.eps_scale;   // keeps the sign: > 0 relative, < 0 absolute
     if (trunc_exact_path(t.m, t.q, t.kmax_tot)) trunc_exact(t, K, pieces, pool, ranks, flags, eps, ctr, dsm);
     else trunc_rand(t, K, pieces, pool, ranks, flags, eps, ctr, dsm, sub, nsub, bar, stt);
 }

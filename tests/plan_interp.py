@@ -27,7 +27,7 @@ VINS = np.dtype([("op", "u1"), ("t0", "u1"), ("t1", "u1"), ("t2", "u1"), ("ta", 
 VTASK = np.dtype([("ins_begin", "<i4"), ("ins_count", "<i4")])
 TTASK = np.dtype([("u_out", "<i8"), ("v_out", "<i8"), ("ws", "<i8"), ("ws_size", "<i8"), ("m", "<i4"),
                   ("q", "<i4"), ("cap", "<i4"), ("rslot", "<i4"), ("piece_begin", "<i4"), ("piece_count", "<i4"),
-                  ("kmax_tot", "<i4"), ("wmax", "<i4"), ("nsub", "<i4"), ("bar", "<i4")])
+                  ("kmax_tot", "<i4"), ("wmax", "<i4"), ("nsub", "<i4"), ("bar", "<i4"), ("eps_scale", "<f8")])
 TPIECE = np.dtype([("u_off", "<i8"), ("v_off", "<i8"), ("u_ld", "<i4"), ("v_ld", "<i4"), ("u_row0", "<i4"),
                    ("u_rows", "<i4"), ("v_row0", "<i4"), ("v_rows", "<i4"), ("w", DIM), ("alpha", "<f8")])
 DGEN = np.dtype([("off", "<i8"), ("r0", "<i4"), ("c0", "<i4"), ("m", "<i4"), ("q", "<i4")])
@@ -235,6 +235,15 @@ class Interp:
             else:
                 raise ValueError(op)
 
+    def run_trunc(self, ph, t):
+        """A truncation at its share eps_scale of the block accuracy (split truncations)."""
+        e = self.eps
+        self.eps = e * float(t["eps_scale"])
+        try:
+            self.trunc(ph, t)
+        finally:
+            self.eps = e
+
     def trunc(self, ph, t):
         m, q = int(t["m"]), int(t["q"])
         As, Bs = [], []
@@ -269,7 +278,7 @@ class Interp:
                 if kind == "v":
                     self.vm(ph, ph.vt[i])
                 else:
-                    self.trunc(ph, ph.tt[i])
+                    self.run_trunc(ph, ph.tt[i])
 
     def run_dag(self, ph):
         n = len(ph.xt)
@@ -291,7 +300,7 @@ class Interp:
             if x["kind"] == 0:
                 self.vm(ph, ph.vt[x["idx"]])
             elif x["sub"] == 0:              # a cooperative truncation runs once (its leader)
-                self.trunc(ph, ph.tt[x["idx"]])
+                self.run_trunc(ph, ph.tt[x["idx"]])
             done += 1
             for s2 in succ[i]:
                 indeg[s2] -= 1
@@ -360,7 +369,7 @@ class InterpRand(Interp):
             Om = self.rng.standard_normal((q, self.RB))
             Y = A @ (B.T @ Om)
             sest = max(sest, float(np.max(np.linalg.norm(Y, axis=0))))   # ~ ||M||_F
-            thr = (self.eps * sest if self.rel_eps else self.eps * self.sigma2) * 4.0   # TR_STOP
+            thr = (self.eps * sest if self.rel_eps else self.eps * self.sigma2) * 1.0   # TR_STOP
             for _ in range(2):                       # BCGS2, first projection (twice)
                 Y = Y - Q @ (Q.T @ Y)
             G = Y.T @ Y                              # pivoted Cholesky-QR of the block
