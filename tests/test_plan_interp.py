@@ -55,6 +55,10 @@ def test_randomized_truncation_algorithm(tmp_path, eps, tol):
     ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), 32, 2.0, eps, kmax=160, seed=0, k=1,
                                          cls=InterpRand)
     np.testing.assert_allclose(ll, oll, rtol=tol)
+    # wide truncations are split into an early partial merge (eps share 1/4) + final step (3/4)
+    P = Plan(str(tmp_path / "plan.bin"))
+    sc = P.chol.tt["eps_scale"]
+    assert np.any(sc == 0.25) and np.sum(sc == 0.25) == np.sum(sc == 0.75)
 
 
 def test_randomized_recompression_of_tall_blocks(tmp_path):
