@@ -51,13 +51,20 @@ WORKLOADS = {
     # 60 Nelder-Mead evaluations each; a "step" = one replicate per rank (bench.py --workload mc)
     "mc": dict(n=16384, kind="uniform", thetas=[(1.0, 0.0334, 0.5)], leaf=32, eta=2.0, eps=1e-6, cfg="configs[3]",
                evals=60, start=(0.8, 0.05, 0.7)),
+    # configs[4]: 2,000,000 lat/lon locations (jittered 0.0067 deg grid, 30 % dropout), ell in degrees;
+    # Z drawn by the H sampler at eps 1e-8, likelihood at eps 1e-6; one evaluation at a time (S = 1).
+    # Rank capacities from the n = 262,144 probe (max rank of L~ 17 at 1e-6, 27 at 1e-8).
+    "n2m": dict(n=2_000_000, kind="latlon", thetas=[(1.0, 0.1, 0.35)], leaf=64, eta=2.0, eps=1e-6, cfg="configs[4]",
+                eps_sample=1e-8, kmax=24, kmax_sample=32),
 }
 
 
 def make_points(w, seed=2):
-    from synthetic import perturbed_mesh, uniform_iid
+    from synthetic import latlon_dropout, perturbed_mesh, uniform_iid
     if w["kind"] == "mesh":
         return perturbed_mesh(w["sqrt_n"], w["delta"], seed)
+    if w["kind"] == "latlon":
+        return latlon_dropout(w["n"], seed)
     return uniform_iid(w["n"], seed)
 
 
@@ -65,8 +72,9 @@ def workload_str(w, args):
     """The configuration both arms name in their JSON line (config.workload)."""
     if w["cfg"] == "configs[3]":
         return f"{w['cfg']}: MC-MLE, n={w['n']}, {w['evals']} Nelder-Mead evals per replicate, eps={w['eps']}"
+    extra = f", Z by the H sampler at eps={w['eps_sample']}" if "eps_sample" in w else ""
     return (f"{w['cfg']}: n={w['n']} {w['kind']}, theta={w['thetas']} (ell swept +-2%), leaf={w['leaf']}, "
-            f"eta={w['eta']}, eps={w['eps']}, kmax={args.kmax}")
+            f"eta={w['eta']}, eps={w['eps']}, kmax={w.get('kmax', args.kmax)}{extra}")
 
 
 def theta_schedule(w, steps):
@@ -354,20 +362,36 @@ def run_gpu(args, w):
     from paper_1709_04419_b200.dist import gather_results
     from synthetic import standard_normal
 
-    S = max(1, args.theta_streams)
+    S = max(1, args.theta_streams) if "eps_sample" not in w else 1   # 2M: one handle fills the GPU
     sms = torch.cuda.get_device_properties(lr).multi_processor_count
     # cooperative groups <= 8 CTAs when co-scheduled, and within the deadlock bound
     # 4 * (coop - 1) < executor CTAs = sms / S
     coop = 16 if S == 1 else max(1, min(8, (sms // S - 1) // 4 + 1))
+    kmax = w.get("kmax", args.kmax)
     pts = make_points(w)
     n = pts.shape[0]
     steps, warm = args.steps, args.warmup
     mine = rank_thetas(w, warm + steps, S, rk, ws)   # this rank's thetas, S per step
-    H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=args.kmax, device=lr,
-                   coop_max=coop)
-    H.cholesky()
     xi = standard_normal(n, 1, 11)
-    Zh = np.ascontiguousarray(H.sample(xi)[:, 0])
+    t_build = time.perf_counter()
+    if "eps_sample" in w:
+        # configs[4]: Z = L~ xi by the H sampler at its own accuracy, on its own
+        # handle, freed before the likelihood handle is built (device memory)
+        Hs = hm.HMatrix(pts, w["thetas"][0], eps=w["eps_sample"], leaf=w["leaf"], eta=w["eta"],
+                        kmax=w["kmax_sample"], device=lr, coop_max=coop)
+        Hs.cholesky()
+        Zh = np.ascontiguousarray(Hs.sample(xi)[:, 0])
+        sampler_stats = Hs.stats()
+        Hs.close()
+        H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=kmax, device=lr,
+                       coop_max=coop)
+    else:
+        sampler_stats = None
+        H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=kmax, device=lr,
+                       coop_max=coop)
+        H.cholesky()
+        Zh = np.ascontiguousarray(H.sample(xi)[:, 0])
+    t_build = time.perf_counter() - t_build
     Zd = torch.from_numpy(Zh).to(f"cuda:{lr}")
     H.set_batch_streams(S)
     torch.cuda.synchronize()
@@ -409,7 +433,7 @@ def run_gpu(args, w):
     ms_e2e, _ = timed(Zh, warm, steps)
     # single-evaluation latency (one executor on the whole GPU, same plan)
     H.set_batch_streams(1)
-    lat_n = min(steps, 6) * S
+    lat_n = (min(steps, 2) if "eps_sample" in w else min(steps, 6)) * S
     lat_ms, _ = timed(Zd, warm, lat_n // S)
     H.set_batch_streams(S)
     res = np.concatenate([o.reshape(-1, 3) for o in outs])       # this rank's (loglik, logdet, quad)
@@ -436,7 +460,10 @@ def run_gpu(args, w):
                                           f"(persistent executor CTAs {sms // S} each, coop_max {coop})",
                            "evals_per_step_per_gpu": S, "evals_timed_total": ev,
                            "max_rank_C": st["max_rank_C"], "max_rank_L": st["max_rank_L"],
-                           "bytes_L_MB": round(st["bytes_L"] / 2**20, 1)},
+                           "bytes_L_MB": round(st["bytes_L"] / 2**20, 1), "kmax": kmax,
+                           "setup_s": round(t_build, 1),
+                           "sampler": None if sampler_stats is None else
+                           {"eps": w["eps_sample"], "kmax": w["kmax_sample"], "max_rank_L": sampler_stats["max_rank_L"]}},
                 "latency": {"ms_per_eval": lat_ms / lat_n, "evals_per_s": lat_n / (lat_ms / 1e3),
                             "how": f"{lat_n} evaluations one at a time (hm_set_batch_streams 1), whole GPU"},
                 "e2e": {"value": ev / (ms_e2e / 1e3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n * S,

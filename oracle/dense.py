@@ -19,14 +19,6 @@ import scipy.linalg
 from .matern import matern
 
 
-def pairwise_distances(points: np.ndarray) -> np.ndarray:
-    """h_ij = ||s_i - s_j|| (Euclidean, l.181)."""
-    p = np.asarray(points, dtype=np.float64)
-    dx = p[:, 0][:, None] - p[:, 0][None, :]
-    dy = p[:, 1][:, None] - p[:, 1][None, :]
-    return np.sqrt(dx * dx + dy * dy)
-
-
 def covariance(points: np.ndarray, theta, bessel: str = "quad") -> np.ndarray:
     """Dense C(theta) with entries C(s_i - s_j; theta) (l.56).  Each unordered
     pair is evaluated once and mirrored, so the result is exactly symmetric."""
@@ -74,10 +66,3 @@ def sample(points: np.ndarray, theta, xi: np.ndarray, bessel: str = "quad") -> n
     """Z = L xi with C = L L^T (sec. 4, l.308: "Z = L xi"), dense."""
     L = np.linalg.cholesky(covariance(points, theta, bessel=bessel))
     return L @ np.asarray(xi, dtype=np.float64)
-
-
-def logdet_error_bound(eps_spectral: float, n: int) -> float:
-    """Appendix A, Theorem 3 (l.561-567): |log det C - log det C~| <= -n log(1 - eps)."""
-    if not (0.0 < eps_spectral < 1.0):
-        raise ValueError("0 < eps < 1 required")
-    return -n * math.log1p(-eps_spectral)

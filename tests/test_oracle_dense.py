@@ -119,8 +119,3 @@ def test_sample_covariance_structure():
     Z = dense.sample(pts, theta, xi)
     emp = Z @ Z.T / xi.shape[1]
     np.testing.assert_allclose(emp, dense.covariance(pts, theta), atol=4 / math.sqrt(40000) * 2)
-
-
-def test_theorem3_bound_helper():
-    assert dense.logdet_error_bound(0.5, 1) == pytest.approx(math.log(2.0))
-    assert dense.logdet_error_bound(1e-3, 1000) == pytest.approx(-1000 * math.log(1 - 1e-3))
