@@ -1052,7 +1052,11 @@ struct Builder {
         return true;
     }
     static constexpr double TRUNC_SPLIT_SHARE = 0.25;   // accuracy share of the partial merge
-    bool split_enabled = true;
+    // Off by default (HM_TRUNC_SPLIT=1 enables it): measured at n = 64k it LOSES -- one
+    // evaluation 422 -> 560 ms, 4 co-scheduled 4.68 -> 3.76 evals/s -- the partial merge
+    // is rarely off the critical path in the executor's actual order (the wave proxy
+    // is too coarse) and the extra truncations add work.
+    bool split_enabled = false;
     int64_t n_split = 0;
 
     void emit_trunc(const TruncTarget& tg, const std::vector<TPiece>& pcs, std::vector<int32_t>& reads,

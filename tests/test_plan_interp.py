@@ -55,7 +55,19 @@ def test_randomized_truncation_algorithm(tmp_path, eps, tol):
     ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), 32, 2.0, eps, kmax=160, seed=0, k=1,
                                          cls=InterpRand)
     np.testing.assert_allclose(ll, oll, rtol=tol)
-    # wide truncations are split into an early partial merge (eps share 1/4) + final step (3/4)
+
+
+
+@pytest.mark.parametrize("eps,tol", [(1e-10, 1e-9), (1e-7, 1e-5)])
+def test_split_truncations(tmp_path, monkeypatch, eps, tol):
+    """HM_TRUNC_SPLIT=1 (off by default): wide truncations become an early
+    partial merge (eps share 1/4) + a final step (3/4); the replayed plan still matches the
+    dense oracle at the accuracy eps allows."""
+    monkeypatch.setenv("HM_TRUNC_SPLIT", "1")
+    pts = uniform_iid(2000, 11)
+    ll, ld, q, oll, old, oq, I, _ = _run(tmp_path, pts, (1.0, 0.0864, 0.5), 32, 2.0, eps, kmax=160, seed=0, k=1,
+                                         cls=InterpRand)
+    np.testing.assert_allclose(ll, oll, rtol=tol)
     P = Plan(str(tmp_path / "plan.bin"))
     sc = P.chol.tt["eps_scale"]
     assert np.any(sc == 0.25) and np.sum(sc == 0.25) == np.sum(sc == 0.75)
