@@ -53,9 +53,10 @@ WORKLOADS = {
                evals=60, start=(0.8, 0.05, 0.7)),
     # configs[4]: 2,000,000 lat/lon locations (jittered 0.0067 deg grid, 30 % dropout), ell in degrees;
     # Z drawn by the H sampler at eps 1e-8, likelihood at eps 1e-6; one evaluation at a time (S = 1).
-    # Rank capacities from the n = 262,144 probe (max rank of L~ 17 at 1e-6, 27 at 1e-8).
+    # Rank capacities: the n = 262,144 probe had max ranks 18 (1e-6) and 28 (1e-8); at 2M the
+    # 1e-8 assembly needs more than 32 (measured HM_ERR_RANK_CAP at kmax 32).
     "n2m": dict(n=2_000_000, kind="latlon", thetas=[(1.0, 0.1, 0.35)], leaf=64, eta=2.0, eps=1e-6, cfg="configs[4]",
-                eps_sample=1e-8, kmax=24, kmax_sample=32),
+                eps_sample=1e-8, kmax=32, kmax_sample=48),
 }
 
 
