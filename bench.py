@@ -54,9 +54,10 @@ WORKLOADS = {
     # configs[4]: 2,000,000 lat/lon locations (jittered 0.0067 deg grid, 30 % dropout), ell in degrees;
     # Z drawn by the H sampler at eps 1e-8, likelihood at eps 1e-6; one evaluation at a time (S = 1).
     # Rank capacities: the n = 262,144 probe had max ranks 18 (1e-6) and 28 (1e-8); at 2M the
-    # 1e-8 assembly needs more than 32 (measured HM_ERR_RANK_CAP at kmax 32).
+    # 1e-8 assembly needs more than 48 (measured HM_ERR_RANK_CAP at kmax 32 and 48): with an
+    # absolute eps the blocks' singular values grow with their point counts (sqrt(m q)).
     "n2m": dict(n=2_000_000, kind="latlon", thetas=[(1.0, 0.1, 0.35)], leaf=64, eta=2.0, eps=1e-6, cfg="configs[4]",
-                eps_sample=1e-8, kmax=32, kmax_sample=48),
+                eps_sample=1e-8, kmax=48, kmax_sample=64),
 }
 
 

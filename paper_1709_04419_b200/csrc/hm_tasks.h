@@ -95,7 +95,10 @@ struct TTask {
 };
 
 // k_trunc algorithm selection and workspace (trunc.cuh; planner sizes the workspace)
-constexpr int TR_EXACT_K = 160;   // static stacked width up to which the exact QR+SVD path runs ...
+#ifndef HM_TR_EXACT_K
+#define HM_TR_EXACT_K 160
+#endif
+constexpr int TR_EXACT_K = HM_TR_EXACT_K;   // static stacked width up to which the exact QR+SVD path runs ...
 constexpr int TR_EXACT_MMAX = 512;   // ... on blocks with at most this many rows and columns: the
                                      // single-CTA Householder QR of a taller factor is HBM-latency
                                      // bound (~25 ms at 8192 x 160); those take the cooperative

@@ -183,6 +183,23 @@ static __device__ __noinline__ void jacobi_svd(double* X, int rows, int n, doubl
 }
 
 
+// jacobi_svd with X (rows x n) and Z (n x n) staged in shared memory when they fit the
+// GEMM staging area (the small SVD is latency-bound; global memory makes it ~10x slower)
+static __device__ __forceinline__ void jacobi_smem(double* X, int rows, int n, double* Z, double* sm, int* s_flag) {
+    if ((int64_t)rows * n + (int64_t)n * n <= GEMM_SMEM_DOUBLES) {
+        double* Xs = sm;
+        double* Zs = sm + rows * n;
+        for (int i = threadIdx.x; i < rows * n; i += blockDim.x) Xs[i] = X[i];
+        __syncthreads();
+        jacobi_svd(Xs, rows, n, Zs, s_flag);
+        for (int i = threadIdx.x; i < rows * n; i += blockDim.x) X[i] = Xs[i];
+        for (int i = threadIdx.x; i < n * n; i += blockDim.x) Z[i] = Zs[i];
+        __syncthreads();
+    } else {
+        jacobi_svd(X, rows, n, Z, s_flag);
+    }
+}
+
 // ---------------------------------------------------------------- exact path
 static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restrict__ pieces, double* __restrict__ pool,
                             int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
@@ -235,7 +252,9 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
         X[i + (int64_t)j * Ka] = s;
     }
     __syncthreads();
-    jacobi_svd(X, Ka, Kb, Z, &s_flag);
+    // the small SVD is latency-bound: staged in shared memory behind `order` when it fits
+    // (Ka x Kb + Kb x Kb doubles, i.e. K <= 68; global memory made it ~10x slower)
+    jacobi_smem(X, Ka, Kb, Z, dsm + ORDER_MAX / 2, &s_flag);
     // singular values = column norms of X
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = warp; j < Kb; j += nw) {
@@ -444,23 +463,6 @@ __device__ __forceinline__ void gram_owned(const TruncWs& W, int m, const double
         Gs[i * TR_RB + j] = a;                     // symmetric: row/col order immaterial
     }
     __syncthreads();
-}
-
-// jacobi_svd with X (rows x n) and Z (n x n) staged in shared memory when they fit the
-// GEMM staging area (the small SVD is latency-bound; global memory makes it ~10x slower)
-static __device__ __forceinline__ void jacobi_smem(double* X, int rows, int n, double* Z, double* sm, int* s_flag) {
-    if ((int64_t)rows * n + (int64_t)n * n <= GEMM_SMEM_DOUBLES) {
-        double* Xs = sm;
-        double* Zs = sm + rows * n;
-        for (int i = threadIdx.x; i < rows * n; i += blockDim.x) Xs[i] = X[i];
-        __syncthreads();
-        jacobi_svd(Xs, rows, n, Zs, s_flag);
-        for (int i = threadIdx.x; i < rows * n; i += blockDim.x) X[i] = Xs[i];
-        for (int i = threadIdx.x; i < n * n; i += blockDim.x) Z[i] = Zs[i];
-        __syncthreads();
-    } else {
-        jacobi_svd(X, rows, n, Z, s_flag);
-    }
 }
 
 // Gram-path truncation: column-pivoted Cholesky of the ell x ell Gram matrix G = W^T W
