@@ -280,6 +280,7 @@ void do_cholesky(hm_handle_s* h) {
     h->assembled = false;   // C~ has been overwritten by L~
     if (f[0]) throw ApiError(HM_ERR_NOT_SPD, "H-Cholesky: " + std::to_string(f[0]) + " non-positive pivot(s)");
     h->factored = true;
+    h->max_rank_L = max_rank(h);
     if (f[1]) throw ApiError(HM_ERR_RANK_CAP, "H-Cholesky: a truncation needed more than kmax ranks");
 }
 
@@ -584,7 +585,6 @@ int hm_cholesky(hm_handle h) {
         if (!h) throw ApiError(HM_ERR_ARG, "null handle");
         DeviceGuard dg(h->device);
         do_cholesky(h);
-        h->max_rank_L = max_rank(h);
         return HM_OK;
     } catch (...) {
         return translate_exception();
