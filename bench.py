@@ -57,7 +57,7 @@ WORKLOADS = {
     # 1e-8 assembly needs more than 48 (measured HM_ERR_RANK_CAP at kmax 32 and 48): with an
     # absolute eps the blocks' singular values grow with their point counts (sqrt(m q)).
     "n2m": dict(n=2_000_000, kind="latlon", thetas=[(1.0, 0.1, 0.35)], leaf=64, eta=2.0, eps=1e-6, cfg="configs[4]",
-                eps_sample=1e-8, kmax=48, kmax_sample=64),
+                eps_sample=1e-8, kmax=32, kmax_sample=64),
 }
 
 
