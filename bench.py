@@ -57,7 +57,7 @@ WORKLOADS = {
     # 1e-8 assembly needs more than 48 (measured HM_ERR_RANK_CAP at kmax 32 and 48): with an
     # absolute eps the blocks' singular values grow with their point counts (sqrt(m q)).
     "n2m": dict(n=2_000_000, kind="latlon", thetas=[(1.0, 0.1, 0.35)], leaf=64, eta=2.0, eps=1e-6, cfg="configs[4]",
-                eps_sample=1e-8, kmax=32, kmax_sample=64),
+                eps_sample=1e-8, kmax=48, kmax_sample=64, adaptive=True),
 }
 
 
@@ -380,13 +380,13 @@ def run_gpu(args, w):
         # configs[4]: Z = L~ xi by the H sampler at its own accuracy, on its own
         # handle, freed before the likelihood handle is built (device memory)
         Hs = hm.HMatrix(pts, w["thetas"][0], eps=w["eps_sample"], leaf=w["leaf"], eta=w["eta"],
-                        kmax=w["kmax_sample"], device=lr, coop_max=coop)
+                        kmax=w["kmax_sample"], device=lr, coop_max=coop, adaptive_cap=w.get("adaptive", False))
         Hs.cholesky()
         Zh = np.ascontiguousarray(Hs.sample(xi)[:, 0])
         sampler_stats = Hs.stats()
         Hs.close()
         H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=kmax, device=lr,
-                       coop_max=coop)
+                       coop_max=coop, adaptive_cap=w.get("adaptive", False))
     else:
         sampler_stats = None
         H = hm.HMatrix(pts, mine[0], eps=w["eps"], leaf=w["leaf"], eta=w["eta"], kmax=kmax, device=lr,
@@ -463,6 +463,7 @@ def run_gpu(args, w):
                            "evals_per_step_per_gpu": S, "evals_timed_total": ev,
                            "max_rank_C": st["max_rank_C"], "max_rank_L": st["max_rank_L"],
                            "bytes_L_MB": round(st["bytes_L"] / 2**20, 1), "kmax": kmax,
+                           "adaptive_cap": bool(w.get("adaptive", False)),
                            "setup_s": round(t_build, 1),
                            "sampler": None if sampler_stats is None else
                            {"eps": w["eps_sample"], "kmax": w["kmax_sample"], "max_rank_L": sampler_stats["max_rank_L"]}},

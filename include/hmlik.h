@@ -70,7 +70,15 @@ typedef struct hm_theta { double sigma2, ell, nu; } hm_theta;
  * (l.474-476, Fig. 7: 1e-3 for C~, 1e-8 for L~); Table 3 (l.483) uses one for
  * both, which is the default.  exec_ctas: CTA cap of the handle's persistent
  * executor from hm_build on (0 = all SMs; as hm_set_exec_grid), so a handle built
- * while other handles' executors run never oversubscribes the SMs.             */
+ * while other handles' executors run never oversubscribes the SMs.
+ * adaptive_cap = 1: rank capacity per low-rank block instead of one kmax --
+ * hm_build first assembles C~ with an assembly-only plan at capacity kmax, then
+ * gives every block min(kmax, 1.5 rank_C~ + 8) and plans the H-Cholesky with
+ * that (less device memory: blocks, H x thin temporaries, workspaces); should a
+ * factor block need more, hm_cholesky grows the capacities (x2, at most 3
+ * times), re-plans, re-assembles at the same theta and factors again.  The
+ * capacities stay fixed for later thetas (HM_ERR_RANK_CAP as usual beyond 3
+ * retries).  0 (default) = kmax for every block.                              */
 typedef struct hm_params {
     double  eps;
     int32_t leaf;
@@ -80,6 +88,7 @@ typedef struct hm_params {
     int32_t coop_max;
     double  eps_chol;
     int32_t exec_ctas;
+    int32_t adaptive_cap;
 } hm_params;
 
 typedef struct hm_handle_s* hm_handle;          /* H-matrix of C(theta) + its factor */

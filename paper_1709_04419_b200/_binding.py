@@ -32,7 +32,7 @@ class Theta(C.Structure):
 class Params(C.Structure):
     _fields_ = [("eps", C.c_double), ("leaf", C.c_int32), ("eta", C.c_double), ("kmax", C.c_int32),
                 ("rel_eps", C.c_int32), ("coop_max", C.c_int32), ("eps_chol", C.c_double),
-                ("exec_ctas", C.c_int32)]
+                ("exec_ctas", C.c_int32), ("adaptive_cap", C.c_int32)]
 
 
 def _load():
@@ -233,7 +233,7 @@ class HMatrix:
 
     def __init__(self, locs, theta, eps: float = 1e-8, leaf: int = 32, eta: float = 2.0, kmax: int = 160,
                  device: int = 0, stream=None, rel_eps: bool = False, coop_max: int = 0, eps_chol: float = 0.0,
-                 exec_ctas: int = 0):
+                 exec_ctas: int = 0, adaptive_cap: bool = False):
         if isinstance(locs, np.ndarray) or not hasattr(locs, "is_cuda"):
             locs = _as_f64(locs)
         lp, ld = ptr_of(locs)
@@ -241,7 +241,7 @@ class HMatrix:
         self.device = int(device)
         self._h = C.c_void_p()
         self.params = Params(float(eps), int(leaf), float(eta), int(kmax), 1 if rel_eps else 0, int(coop_max),
-                             float(eps_chol), int(exec_ctas))
+                             float(eps_chol), int(exec_ctas), 1 if adaptive_cap else 0)
         rc = lib.hm_build(lp, ld, self.n, Theta(*theta), self.params, int(device),
                           C.c_void_p(stream) if stream else None, C.byref(self._h))
         check(rc)

@@ -58,6 +58,12 @@ void check_theta(const hm_theta& th) {
 DevBuf::~DevBuf() {
     if (p) cudaFree(p);
 }
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
 void DevBuf::alloc(size_t b) {
     if (b <= bytes && p) return;
     if (p) cudaFree(p);

@@ -26,6 +26,7 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf();
     void alloc(size_t b);
+    void release();   // free now (alloc keeps a larger buffer)
     template <class T>
     T* as() const { return (T*)p; }
 };

@@ -89,6 +89,8 @@ struct hm_handle_s {
     // hm_loglik_batch: S - 1 sibling executors on the same tree + plan (own pool, stream)
     std::vector<std::unique_ptr<hm_handle_s>> subs;
     int batch_streams = 0;   // 0 = auto (hm_set_batch_streams)
+    std::vector<int32_t> cap_hint;   // adaptive rank capacities per plan block (hm_params.adaptive_cap)
+    int cap_retries = 0;
     ~hm_handle_s() {
         if (pin_z) cudaFreeHost(pin_z);
         if (pin_out) cudaFreeHost(pin_out);
@@ -158,6 +160,9 @@ struct Launch {
         h->evlog.push_back({f, idx});
     }
 };
+
+void plan_to_fit(hm_handle_s* h);
+void setup_device(hm_handle_s* h);
 
 void run_phase(hm_handle_s* h, const DPhase& d) {
     const Phase& p = *d.ph;
@@ -281,6 +286,19 @@ void do_cholesky(hm_handle_s* h) {
     if (f[0]) throw ApiError(HM_ERR_NOT_SPD, "H-Cholesky: " + std::to_string(f[0]) + " non-positive pivot(s)");
     h->factored = true;
     h->max_rank_L = max_rank(h);
+    if (f[1] && !h->cap_hint.empty() && h->cap_retries < 3) {
+        // adaptive capacities too small for the factor: grow them (x2, up to kmax), re-plan,
+        // re-assemble at the same theta and factor again
+        ++h->cap_retries;
+        for (auto& c : h->cap_hint)
+            if (c > 0) c = std::min(h->prm.kmax, (2 * c + 3) & ~3);
+        h->pool.release();
+        plan_to_fit(h);
+        setup_device(h);
+        do_assemble(h, h->theta);
+        do_cholesky(h);
+        return;
+    }
     if (f[1]) throw ApiError(HM_ERR_RANK_CAP, "H-Cholesky: a truncation needed more than kmax ranks");
 }
 
@@ -350,6 +368,29 @@ double plan_device_bytes(const Plan& P) {
     return b + 8.0 * ((double)P.dgen.size() + (double)P.aca.size()) * 4.0;
 }
 
+// Adaptive capacity of a block whose C~ rank is r: 1.5 r + 8, a multiple of 4.
+int32_t adaptive_cap_of(int r) { return ((r + r / 2 + 8) + 3) & ~3; }
+
+// Plan the handle's H-Cholesky (with its capacity hints).  Device memory: if the pool (with
+// the temporaries' arena planned for parallelism) and the task lists do not fit, plan again
+// with an arena budget -- memory is then recycled even where that lengthens the critical
+// path (plan.h build_plan).
+void plan_to_fit(hm_handle_s* h) {
+    const hm_params& prm = h->prm;
+    const std::vector<int32_t>* hint = h->cap_hint.empty() ? nullptr : &h->cap_hint;
+    build_plan(h->T, prm.kmax, h->P, prm.coop_max, INT64_MAX, hint);
+    size_t fr = 0, tot = 0;
+    HM_CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    const double avail = 0.92 * ((double)fr + (double)h->pool.bytes) - plan_device_bytes(h->P);
+    if (8.0 * (double)h->P.pool_total > avail) {
+        const double budget = avail / 8.0 - (double)(h->P.pool_total - h->P.arena_size);
+        if (budget < (double)(int64_t(1) << 24))
+            throw ApiError(HM_ERR_OOM, "H-matrix storage does not fit in device memory (" +
+                                           std::to_string(8e-9 * h->P.pool_total) + " GB needed)");
+        build_plan(h->T, prm.kmax, h->P, prm.coop_max, (int64_t)budget, hint);
+    }
+}
+
 // Device side of a handle whose tree and plan are built: pool, task lists, schedules.
 void setup_device(hm_handle_s* h) {
     vm_set_attr();
@@ -407,6 +448,7 @@ hm_handle_s* clone_handle(const hm_handle_s* p) {
     HM_CUDA_TRY(cudaEventCreate(&h->ev[1]));
     h->T = p->T;
     h->P = p->P;
+    h->cap_hint = p->cap_hint;
     setup_device(h.get());
     HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     return h.release();
@@ -495,6 +537,7 @@ extern "C" {
 int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta theta, hm_params params, int32_t device,
              void* stream, hm_handle* out) {
     hm_handle_s* h = nullptr;
+    bool probing = false;   // adaptive capacities: a rank cap in the probe is fatal (no factor plan yet)
     try {
         if (!locs || !out) throw ApiError(HM_ERR_ARG, "null pointer");
         if (n < 1) throw ApiError(HM_ERR_ARG, "n >= 1 required");
@@ -508,6 +551,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (params.coop_max > TR_COOP_MAX) throw ApiError(HM_ERR_ARG, "coop_max <= 32 required");
         if (params.kmax > TR_LMAX - TR_RB) throw ApiError(HM_ERR_ARG, "kmax <= 240 required");
         if (params.exec_ctas < 0) throw ApiError(HM_ERR_ARG, "exec_ctas >= 0 required");
+        if (params.adaptive_cap < 0 || params.adaptive_cap > 1) throw ApiError(HM_ERR_ARG, "adaptive_cap must be 0 or 1");
         check_theta(theta);
         DeviceGuard dg(device);
         h = new hm_handle_s();
@@ -532,30 +576,30 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
             hp = hl.data();
         }
         build_tree(hp, n, params.leaf, params.eta, h->T);
-        build_plan(h->T, params.kmax, h->P, params.coop_max);
-        {
-            // Device memory: if the pool (with the temporaries' arena planned for
-            // parallelism) and the task lists do not fit, plan again with an arena
-            // budget -- memory is then recycled even where that lengthens the
-            // critical path (plan.h build_plan).
-            size_t fr = 0, tot = 0;
-            HM_CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-            const double avail = 0.92 * (double)fr - plan_device_bytes(h->P);
-            if (8.0 * (double)h->P.pool_total > avail) {
-                const double budget = avail / 8.0 - (double)(h->P.pool_total - h->P.arena_size);
-                if (budget < (double)(int64_t(1) << 24))
-                    throw ApiError(HM_ERR_OOM, "H-matrix storage does not fit in device memory (" +
-                                                   std::to_string(8e-9 * h->P.pool_total) + " GB needed)");
-                build_plan(h->T, params.kmax, h->P, params.coop_max, (int64_t)budget);
-            }
+        if (params.adaptive_cap) {
+            probing = true;
+            // rank probe: assemble C~ at capacity kmax with an assembly-only plan, then size
+            // every low-rank block from its C~ rank (the factor's ranks run somewhat higher)
+            build_plan(h->T, params.kmax, h->P, params.coop_max, INT64_MAX, nullptr, true);
+            setup_device(h);
+            do_assemble(h, theta);
+            h->cap_hint.assign(h->P.bs.size(), 0);
+            // HM_ADAPTIVE_SCALE (tests): scale the capacities down to exercise the regrowth path
+            const double sc = std::getenv("HM_ADAPTIVE_SCALE") ? std::atof(std::getenv("HM_ADAPTIVE_SCALE")) : 1.0;
+            for (size_t b = 0; b < h->P.bs.size(); ++b)
+                if (h->P.bs[b].kind == ST_LR)
+                    h->cap_hint[b] = std::max(1, (int)(sc * adaptive_cap_of(h->h_ranks[h->P.bs[b].rslot])));
+            h->pool.release();
+            probing = false;
         }
+        plan_to_fit(h);
         setup_device(h);
         do_assemble(h, theta);
         *out = h;
         return HM_OK;
     } catch (...) {
         int rc = translate_exception();
-        if (rc == HM_ERR_RANK_CAP && h) {   // handle is usable; report the cap
+        if (rc == HM_ERR_RANK_CAP && h && !probing) {   // handle is usable; report the cap
             *out = h;
             return rc;
         }

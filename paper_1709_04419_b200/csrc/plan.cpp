@@ -1271,7 +1271,8 @@ std::string Plan::summary() const {
     return buf;
 }
 
-void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t arena_budget) {
+void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t arena_budget,
+                const std::vector<int32_t>* cap_hint, bool assembly_only) {
     // mixed-depth leaves (n / 2^l straddling n_min) and leaves above one 64 x 64 tile
     // (n_min up to 128) are planned on the refined storage tree (tree.h refine_for_plan):
     // same C~, dense blocks split into equal-depth tile-sized sub-blocks
@@ -1335,6 +1336,7 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
         } else {
             s.kind = ST_LR;
             s.cap = std::min(kmax, std::min(s.m, s.p));
+            if (cap_hint && b < (int32_t)cap_hint->size() && (*cap_hint)[b] > 0) s.cap = std::min(s.cap, (*cap_hint)[b]);
             s.rslot = P.n_slots++;
             s.u_off = bld.alloc((int64_t)s.m * s.cap);
             s.v_off = bld.alloc((int64_t)s.p * s.cap);
@@ -1418,23 +1420,25 @@ void build_plan(const Tree& T0, int32_t kmax, Plan& P, int32_t coop_max, int64_t
     bld.begin_phase(P.recompress);
     for (int32_t b : lr_order) bld.flush_lr(b, true);
     bld.end_phase();
-    // H-Cholesky
-    bld.begin_phase(P.chol);
-    bld.n_tasks = 0;
-    bld.chol(0);
-    P.n_tasks_chol = bld.n_tasks;
-    bld.end_phase();
-    for (auto& pd : bld.pend)
-        if (!pd.prods.empty() || !pd.pieces.empty()) throw std::logic_error("planner: unapplied pending update");
-    // forward solve and sampler on the z buffer (rows = root cluster, tree order)
-    Thin Z;
-    Z.off = P.z_off; Z.ld = (int32_t)T.n; Z.cluster = 0; Z.cols = P.zw; Z.slot = P.z_slot; Z.res0 = z_res0;
-    bld.begin_phase(P.solve);
-    bld.fsolve(0, Z);
-    bld.end_phase();
-    bld.begin_phase(P.lmul);
-    bld.lmul(0, Z);
-    bld.end_phase();
+    if (!assembly_only) {   // (assembly-only plans: rank probes of hm_build's adaptive capacities)
+        // H-Cholesky
+        bld.begin_phase(P.chol);
+        bld.n_tasks = 0;
+        bld.chol(0);
+        P.n_tasks_chol = bld.n_tasks;
+        bld.end_phase();
+        for (auto& pd : bld.pend)
+            if (!pd.prods.empty() || !pd.pieces.empty()) throw std::logic_error("planner: unapplied pending update");
+        // forward solve and sampler on the z buffer (rows = root cluster, tree order)
+        Thin Z;
+        Z.off = P.z_off; Z.ld = (int32_t)T.n; Z.cluster = 0; Z.cols = P.zw; Z.slot = P.z_slot; Z.res0 = z_res0;
+        bld.begin_phase(P.solve);
+        bld.fsolve(0, Z);
+        bld.end_phase();
+        bld.begin_phase(P.lmul);
+        bld.lmul(0, Z);
+        bld.end_phase();
+    }
     for (const auto& a : bld.tmps)
         if (a.refs != 0) throw std::logic_error("planner: live temporary at the end of planning");
     P.n_split = bld.n_split;

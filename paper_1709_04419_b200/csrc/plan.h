@@ -102,7 +102,11 @@ constexpr int32_t TILE_MAX_LEAF = 64;
 // halve down to TILE_MAX_LEAF without empty clusters).
 // arena_budget: doubles the H x thin temporaries may occupy before recycling memory
 // whose last users finish late (longer critical path, smaller footprint).
+// cap_hint (optional, indexed like Plan::bs): per-block rank capacity below kmax (adaptive
+// capacities, hm_params.adaptive_cap).  assembly_only: plan only the assembly and the
+// recompression (a rank probe), no Cholesky / solve / sampler phases.
 void build_plan(const Tree& T, int32_t kmax, Plan& P, int32_t coop_max = TR_COOP_DEFAULT,
-                int64_t arena_budget = INT64_MAX);
+                int64_t arena_budget = INT64_MAX, const std::vector<int32_t>* cap_hint = nullptr,
+                bool assembly_only = false);
 
 }  // namespace hm

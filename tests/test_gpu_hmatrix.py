@@ -313,3 +313,22 @@ def test_loglik_multi_different_locations(hm):
     with pytest.raises(hm.HMError):
         _, rc = hm.loglik_multi(H16, [ths[0]] * 4, [Z16] * 4)
         hm._binding.check(rc)
+
+
+@pytest.mark.parametrize("scale", [1.0, 0.25])
+def test_adaptive_capacities(hm, config0, monkeypatch, scale):
+    """hm_params.adaptive_cap: rank capacities sized per block from the assembled C~'s ranks
+    (rank probe with an assembly-only plan); at scale 0.25 (test hook HM_ADAPTIVE_SCALE) the
+    capacities are too small for the factor and hm_cholesky must grow them, re-plan and
+    factor again.  Either way the likelihood meets the north-star bar and stays equal over
+    repeated thetas."""
+    monkeypatch.setenv("HM_ADAPTIVE_SCALE", str(scale))
+    pts, theta, Z, (oll, old, oq) = config0
+    H = hm.HMatrix(pts, theta, eps=1e-8, leaf=32, eta=2.0, kmax=64, adaptive_cap=True)
+    H.cholesky()
+    got = H.loglik(Z)[0, 0]
+    assert abs(got - oll) / abs(oll) <= 1e-6
+    H.assemble(theta)
+    H.cholesky()
+    assert H.loglik(Z)[0, 0] == got
+    assert H.stats()["max_rank_L"] <= 64
