@@ -238,7 +238,18 @@ int max_rank(hm_handle_s* h) {
     return mx;
 }
 
-void do_assemble(hm_handle_s* h, hm_theta th) {
+// grow adaptive capacities after an overflow and re-plan (the handle keeps theta)
+void regrow_caps(hm_handle_s* h) {
+    ++h->cap_retries;
+    for (auto& c : h->cap_hint)
+        if (c > 0) c = std::min(h->prm.kmax, (2 * c + 3) & ~3);
+    h->pool.release();
+    plan_to_fit(h);
+    setup_device(h);
+}
+
+// aca_ranks (rank probe): receives every slot's rank after ACA, before the recompression
+void do_assemble(hm_handle_s* h, hm_theta th, std::vector<int>* aca_ranks = nullptr) {
     check_theta(th);
     h->theta = th;
     h->eps_k = h->abs_eps ? -h->prm.eps * th.sigma2 : h->prm.eps;
@@ -258,6 +269,12 @@ void do_assemble(hm_handle_s* h, hm_theta th) {
         launch_aca(h->aca.as<AcaTask>(), (int)h->P.aca.size(), h->pts.as<double>(), h->pool.as<double>(),
                    h->ranks.as<int>(), h->flags.as<int>(), h->mp, 0.25 * h->eps_k, h->ctr.as<double>(), h->stream);
     }
+    if (aca_ranks) {
+        aca_ranks->resize(h->P.n_slots);
+        HM_CUDA_TRY(cudaMemcpyAsync(aca_ranks->data(), h->ranks.p, sizeof(int) * h->P.n_slots, cudaMemcpyDeviceToHost,
+                                    h->stream));
+        HM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
     run_phase(h, h->rec);
     HM_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
     int f[4];
@@ -266,6 +283,11 @@ void do_assemble(hm_handle_s* h, hm_theta th) {
     h->assembled = true;
     h->factored = false;
     h->max_rank_C = max_rank(h);
+    if (f[1] && !h->cap_hint.empty() && h->cap_retries < 3) {   // adaptive capacities: grow, retry
+        regrow_caps(h);
+        do_assemble(h, th);
+        return;
+    }
     if (f[1]) throw ApiError(HM_ERR_RANK_CAP, "assembly: a block needs more than kmax = " +
                                                   std::to_string(h->prm.kmax) + " ranks at this eps");
 }
@@ -289,12 +311,7 @@ void do_cholesky(hm_handle_s* h) {
     if (f[1] && !h->cap_hint.empty() && h->cap_retries < 3) {
         // adaptive capacities too small for the factor: grow them (x2, up to kmax), re-plan,
         // re-assemble at the same theta and factor again
-        ++h->cap_retries;
-        for (auto& c : h->cap_hint)
-            if (c > 0) c = std::min(h->prm.kmax, (2 * c + 3) & ~3);
-        h->pool.release();
-        plan_to_fit(h);
-        setup_device(h);
+        regrow_caps(h);
         do_assemble(h, h->theta);
         do_cholesky(h);
         return;
@@ -582,13 +599,18 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
             // every low-rank block from its C~ rank (the factor's ranks run somewhat higher)
             build_plan(h->T, params.kmax, h->P, params.coop_max, INT64_MAX, nullptr, true);
             setup_device(h);
-            do_assemble(h, theta);
+            std::vector<int> aca_r;
+            do_assemble(h, theta, &aca_r);
             h->cap_hint.assign(h->P.bs.size(), 0);
             // HM_ADAPTIVE_SCALE (tests): scale the capacities down to exercise the regrowth path
             const double sc = std::getenv("HM_ADAPTIVE_SCALE") ? std::atof(std::getenv("HM_ADAPTIVE_SCALE")) : 1.0;
             for (size_t b = 0; b < h->P.bs.size(); ++b)
-                if (h->P.bs[b].kind == ST_LR)
-                    h->cap_hint[b] = std::max(1, (int)(sc * adaptive_cap_of(h->h_ranks[h->P.bs[b].rslot])));
+                if (h->P.bs[b].kind == ST_LR) {
+                    // room for the factor's rank (1.5 r + 8) and for ACA's iterations before recompression
+                    const int rs = h->P.bs[b].rslot;
+                    const int c = std::max(adaptive_cap_of(h->h_ranks[rs]), (aca_r[rs] + 2 + 3) & ~3);
+                    h->cap_hint[b] = std::max(1, (int)(sc * c));
+                }
             h->pool.release();
             probing = false;
         }
