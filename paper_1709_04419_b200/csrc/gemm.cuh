@@ -40,9 +40,18 @@ struct GOp {
 };
 __device__ __forceinline__ GOp gop(const double* p, int64_t ld, bool trans) { return GOp{p, ld, trans}; }
 
+// Staged chunk layouts (doubles): an operand whose memory is contiguous along the
+// tile dimension (A not transposed, B transposed) is staged [k][i] with ld BM + 4,
+// one contiguous along k (A transposed, B not) is staged [i][k] with ld BK + 4.
+// Both keep rows 16-byte aligned for 16-byte cp.async and make every DMMA
+// fragment load conflict-free per half-warp (bank offsets 8t + 2g resp. 8g + 2t).
+template <int BM>
+constexpr int gemm_stage_doubles() {
+    return (GM_BKC * (BM + 4) > BM * (GM_BKC + 4)) ? GM_BKC * (BM + 4) : BM * (GM_BKC + 4);
+}
 template <int BM, int BN>
 constexpr int gemm_smem_doubles() {
-    return GM_NSC * (GM_BKC * (BM + 1) + GM_BKC * (BN + 1));
+    return GM_NSC * (gemm_stage_doubles<BM>() + gemm_stage_doubles<BN>());
 }
 
 __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, bool valid) {
@@ -50,57 +59,70 @@ __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, b
     const int sz = valid ? 8 : 0;                        // 0 -> zero fill
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
+// 16-byte copy of nbytes (0, 8 or 16) source bytes, the rest zero-filled
+__device__ __forceinline__ void cp_async16(double* dst_smem, const double* src, int nbytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(nbytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// One operand's share of a chunk copy: NP element pairs per thread, each pair two
+// elements adjacent in memory (one 16-byte cp.async when the operand is 16-byte
+// aligned with an even ld, else two 8-byte copies); elements outside the matrix
+// are zero-filled.  Operand rows [r0, r0 + BD) of R, contiguous along k when kc.
+template <int BD, int NP>
+__device__ __forceinline__ void gemm_issue(const double* p, int64_t ld, bool kc, bool vec, int r0, int R, int k0, int Kd,
+                                           double* stage) {
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+        const int pr = threadIdx.x + e * 256;
+        if (pr >= GM_BKC * BD / 2) break;
+        int r, k, so, n;   // n: valid elements of the pair
+        if (kc) {
+            k = 2 * (pr % (GM_BKC / 2)); r = pr / (GM_BKC / 2); so = r * (GM_BKC + 4) + k;
+            const int gk = k0 + k;
+            n = (r0 + r >= R) ? 0 : (gk + 1 < Kd ? 2 : (gk < Kd ? 1 : 0));
+        } else {
+            r = 2 * (pr % (BD / 2)); k = pr / (BD / 2); so = k * (BD + 4) + r;
+            const int gr = r0 + r;
+            n = (k0 + k >= Kd) ? 0 : (gr + 1 < R ? 2 : (gr < R ? 1 : 0));
+        }
+        const double* src = n ? p + (kc ? (int64_t)(r0 + r) * ld + (k0 + k) : (r0 + r) + (int64_t)(k0 + k) * ld) : p;
+        if (vec) {
+            cp_async16(stage + so, src, 8 * n);
+        } else {
+            cp_async8(stage + so, src, n >= 1);
+            cp_async8(stage + so + 1, n >= 2 ? src + 1 : p, n >= 2);
+        }
+    }
+}
 
 template <int BM, int BN, int WM, int WN>
 __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta, double* C,
                          int64_t ldc, int first, int step, double* smem) {
     static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
     constexpr int FM = WM / 8, FN = WN / 8;              // DMMA blocks per warp
-    constexpr int LA = BM + 1, LB = BN + 1;              // padded leading dims of the staged chunks
-    constexpr int SA = GM_BKC * LA, SB = GM_BKC * LB;      // doubles per stage
-    constexpr int NA = (GM_BKC * BM + 255) / 256, NB = (GM_BKC * BN + 255) / 256;
-    double* As = smem;                                   // [stage][k][i]
-    double* Bs = smem + GM_NSC * SA;                      // [stage][k][j]
-    const bool tA = A.trans, tB = B.trans;
+    constexpr int SA = gemm_stage_doubles<BM>(), SB = gemm_stage_doubles<BN>();   // doubles per stage
+    constexpr int NPA = (GM_BKC * BM / 2 + 255) / 256, NPB = (GM_BKC * BN / 2 + 255) / 256;
+    double* As = smem;                                   // [stage] A chunk
+    double* Bs = smem + GM_NSC * SA;                     // [stage] B chunk
+    // A^T is contiguous along k, A along rows; B along k, B^T along columns
+    const bool kcA = A.trans, kcB = !B.trans;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
     const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
     const int nk = (Kd + GM_BKC - 1) / GM_BKC;
+    // staged strides (doubles) of the tile row and of k for the fragment loads
+    const int ars = kcA ? GM_BKC + 4 : 1, aks = kcA ? 1 : BM + 4;
+    const int brs = kcB ? GM_BKC + 4 : 1, bks = kcB ? 1 : BN + 4;
+    const int afo = t * aks + (wm + g) * ars, bfo = t * bks + (wn + g) * brs;
+    const bool vA = ((reinterpret_cast<uintptr_t>(A.p) & 15) == 0) && ((A.ld & 1) == 0);
+    const bool vB = ((reinterpret_cast<uintptr_t>(B.p) & 15) == 0) && ((B.ld & 1) == 0);
     for (int tile = first; tile < tm * tn; tile += step) {
         const int i0 = (tile % tm) * BM, j0 = (tile / tm) * BN;
-        auto issue = [&](int kc) {                       // chunk kc -> stage kc % NS
-            const int k0 = kc * GM_BKC;
-            double* as = As + (kc % GM_NSC) * SA;
-            double* bs = Bs + (kc % GM_NSC) * SB;
-#pragma unroll
-            for (int e = 0; e < NA; ++e) {
-                const int idx = threadIdx.x + e * 256;
-                if (idx < GM_BKC * BM) {
-                    int i, k;
-                    if (tA) { k = idx % GM_BKC; i = idx / GM_BKC; } else { i = idx % BM; k = idx / BM; }
-                    const int gi = i0 + i, gk = k0 + k;
-                    const bool ok = gi < M && gk < Kd;
-                    cp_async8(as + k * LA + i, ok ? (tA ? A.p + gk + (int64_t)gi * A.ld : A.p + gi + (int64_t)gk * A.ld) : A.p,
-                              ok);
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < NB; ++e) {
-                const int idx = threadIdx.x + e * 256;
-                if (idx < GM_BKC * BN) {
-                    int j, k;
-                    if (tB) { j = idx % BN; k = idx / BN; } else { k = idx % GM_BKC; j = idx / GM_BKC; }
-                    const int gj = j0 + j, gk = k0 + k;
-                    const bool ok = gj < N && gk < Kd;
-                    cp_async8(bs + k * LB + j, ok ? (tB ? B.p + gj + (int64_t)gk * B.ld : B.p + gk + (int64_t)gj * B.ld) : B.p,
-                              ok);
-                }
-            }
-        };
         double acc[FM][FN][2];
 #pragma unroll
         for (int a = 0; a < FM; ++a)
@@ -109,23 +131,30 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
         __syncthreads();                                 // previous tile's readers are done with the stages
 #pragma unroll
         for (int s = 0; s < GM_NSC - 1; ++s) {
-            if (s < nk) issue(s);
+            if (s < nk) {
+                gemm_issue<BM, NPA>(A.p, A.ld, kcA, vA, i0, M, s * GM_BKC, Kd, As + s * SA);
+                gemm_issue<BN, NPB>(B.p, B.ld, kcB, vB, j0, N, s * GM_BKC, Kd, Bs + s * SB);
+            }
             cp_async_commit();
         }
         for (int kc = 0; kc < nk; ++kc) {
             cp_async_wait<GM_NSC - 2>();
             __syncthreads();
-            if (kc + GM_NSC - 1 < nk) issue(kc + GM_NSC - 1);
+            if (kc + GM_NSC - 1 < nk) {
+                const int sn = (kc + GM_NSC - 1) % GM_NSC;
+                gemm_issue<BM, NPA>(A.p, A.ld, kcA, vA, i0, M, (kc + GM_NSC - 1) * GM_BKC, Kd, As + sn * SA);
+                gemm_issue<BN, NPB>(B.p, B.ld, kcB, vB, j0, N, (kc + GM_NSC - 1) * GM_BKC, Kd, Bs + sn * SB);
+            }
             cp_async_commit();
-            const double* as = As + (kc % GM_NSC) * SA;
-            const double* bs = Bs + (kc % GM_NSC) * SB;
+            const double* as = As + (kc % GM_NSC) * SA + afo;
+            const double* bs = Bs + (kc % GM_NSC) * SB + bfo;
 #pragma unroll
             for (int kk = 0; kk < GM_BKC; kk += 4) {
                 double af[FM], bf[FN];
 #pragma unroll
-                for (int a = 0; a < FM; ++a) af[a] = as[(kk + t) * LA + wm + a * 8 + g];
+                for (int a = 0; a < FM; ++a) af[a] = as[kk * aks + a * 8 * ars];
 #pragma unroll
-                for (int b = 0; b < FN; ++b) bf[b] = bs[(kk + t) * LB + wn + b * 8 + g];
+                for (int b = 0; b < FN; ++b) bf[b] = bs[kk * bks + b * 8 * brs];
 #pragma unroll
                 for (int a = 0; a < FM; ++a)
 #pragma unroll

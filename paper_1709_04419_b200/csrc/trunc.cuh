@@ -417,8 +417,9 @@ __device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int
     bool first = true;
     for (int c = sub; c < nchm; c += nsub) {
         const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        gemm_short(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
-                   gsm);
+        // (128 x 16 tiles: one per 128 basis columns, not one per 16 of the 16 x 128 shape)
+        gemm_narrow(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
+                    gsm);
         first = false;
     }
     if (first)
@@ -728,32 +729,47 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         // pivoted Cholesky (redundant, identical in every CTA): accept pivots above
         // max(thr, 1e-4 * largest) so R stays well conditioned (cond <= 1e4); weaker
         // directions are picked up by the next round's probes
-        if (threadIdx.x == 0) {
-            double d0 = 0.0;
-            for (int j = 0; j < TR_RB; ++j) { piv[j] = j; d0 = fmax(d0, Gs[j * TR_RB + j]); }
-            s_maxn = sqrt(fmax(d0, 0.0));
+        // (warp 0: lanes own pivot candidates / Schur entries; same arithmetic, per entry, as a
+        // serial loop, ties of the pivot search to the lowest index)
+        if (warp == 0) {
+            double dg = (lane < TR_RB) ? Gs[lane * TR_RB + lane] : 0.0;
+            if (lane < TR_RB) piv[lane] = lane;
+            double d0 = dg;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
             const double cut = fmax(thr * thr, 1e-8 * d0);
+            if (lane == 0) s_maxn = sqrt(fmax(d0, 0.0));
+            __syncwarp();
             int na = 0;
             for (int k = 0; k < TR_RB && ell + k < L; ++k) {
-                int jb = k;
-                for (int j = k + 1; j < TR_RB; ++j)
-                    if (Gs[piv[j] * TR_RB + piv[j]] > Gs[piv[jb] * TR_RB + piv[jb]]) jb = j;
-                const int tmp = piv[k]; piv[k] = piv[jb]; piv[jb] = tmp;
+                // argmax over j >= k of the remaining diagonal (lowest j on ties)
+                double bv = (lane >= k && lane < TR_RB) ? Gs[piv[lane] * TR_RB + piv[lane]] : -DBL_MAX;
+                int bj = (lane >= k && lane < TR_RB) ? lane : TR_RB;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                    if (ov > bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+                }
+                __syncwarp();
+                if (lane == 0) { const int tmp = piv[k]; piv[k] = piv[bj]; piv[bj] = tmp; }
+                __syncwarp();
                 const int pk = piv[k];
                 const double d = Gs[pk * TR_RB + pk];
                 if (!(d > cut)) break;
                 const double rkk = sqrt(d);
-                Rs[k * TR_RB + k] = rkk;
-                for (int j = k + 1; j < TR_RB; ++j) Rs[k * TR_RB + j] = Gs[pk * TR_RB + piv[j]] / rkk;
-                for (int i = k + 1; i < TR_RB; ++i)        // trailing Schur complement (pivoted indices)
-                    for (int j = i; j < TR_RB; ++j) {
-                        const double v = Gs[piv[i] * TR_RB + piv[j]] - Rs[k * TR_RB + i] * Rs[k * TR_RB + j];
-                        Gs[piv[i] * TR_RB + piv[j]] = v;
-                        Gs[piv[j] * TR_RB + piv[i]] = v;
-                    }
+                if (lane == k) Rs[k * TR_RB + k] = rkk;
+                if (lane > k && lane < TR_RB) Rs[k * TR_RB + lane] = Gs[pk * TR_RB + piv[lane]] / rkk;
+                __syncwarp();
+                const int rem = TR_RB - k - 1;   // trailing Schur complement (pivoted indices), both triangles
+                for (int idx = lane; idx < rem * rem; idx += 32) {
+                    const int i = k + 1 + idx % rem, j = k + 1 + idx / rem;
+                    Gs[piv[i] * TR_RB + piv[j]] -= Rs[k * TR_RB + i] * Rs[k * TR_RB + j];
+                }
+                __syncwarp();
                 ++na;
             }
-            s_na = na;
+            if (lane == 0) s_na = na;
         }
         __syncthreads();
         const int na = s_na;
@@ -780,17 +796,18 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             if (ell > 0) proj_owned(W, m, ell, L, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm);
             gram_owned(W, m, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm, Gs);
             // CholQR of the (nearly orthonormal) new block: Qn <- Qn chol(Qn^T Qn)^-1
-            if (threadIdx.x == 0) {
+            // (warp 0: lane j forms row k's entry j; sums in the order l = 0 .. k-1)
+            if (warp == 0) {
                 for (int k = 0; k < na; ++k) {
-                    double d = Gs[k * TR_RB + k];
-                    for (int l = 0; l < k; ++l) d -= Rs[l * TR_RB + k] * Rs[l * TR_RB + k];
-                    const double rkk = sqrt(fmax(d, 1e-300));
-                    Rs[k * TR_RB + k] = rkk;
-                    for (int j = k + 1; j < na; ++j) {
-                        double v = Gs[k * TR_RB + j];
-                        for (int l = 0; l < k; ++l) v -= Rs[l * TR_RB + k] * Rs[l * TR_RB + j];
-                        Rs[k * TR_RB + j] = v / rkk;
+                    double v = 0.0;
+                    if (lane >= k && lane < na) {
+                        v = Gs[k * TR_RB + lane];
+                        for (int l = 0; l < k; ++l) v -= Rs[l * TR_RB + k] * Rs[l * TR_RB + lane];
                     }
+                    const double rkk = sqrt(fmax(__shfl_sync(0xffffffffu, v, k), 1e-300));
+                    if (lane == k) Rs[k * TR_RB + k] = rkk;
+                    if (lane > k && lane < na) Rs[k * TR_RB + lane] = v / rkk;
+                    __syncwarp();
                 }
             }
             __syncthreads();

@@ -67,6 +67,12 @@ int main() {
     run<0>("wide", 256, 48, 1700, false, true, 1);        // F2: W = Bst P
     run<2>("short", 112, 16, 4096, true, false, 1);       // proj: C = Q^T Y
     run<0>("wide", 4096, 64, 1700, false, true, 26);      // big F2 on a group
+    // ragged / odd leading dimensions (8-byte fallback copies, half-valid pairs)
+    run<0>("wide", 255, 37, 301, false, false, 4);
+    run<0>("wide", 255, 37, 301, true, true, 4);
+    run<1>("narrow", 130, 16, 257, true, false, 2);
+    run<2>("short", 16, 131, 255, false, true, 2);
+    run<1>("narrow", 80, 16, 64, true, false, 1);         // proj: Q^T Y on one row chunk
     run<0>("wide", 8192, 8192, 64, false, true, 148);     // throughput check
     run<0>("wide", 2048, 2048, 2048, false, false, 148);
     return 0;
