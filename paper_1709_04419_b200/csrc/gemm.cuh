@@ -68,61 +68,83 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// One operand's share of a chunk copy: NP element pairs per thread, each pair two
-// elements adjacent in memory (one 16-byte cp.async when the operand is 16-byte
-// aligned with an even ld, else two 8-byte copies); elements outside the matrix
-// are zero-filled.  Operand rows [r0, r0 + BD) of R, contiguous along k when kc.
-template <int BD, int NP>
-__device__ __forceinline__ void gemm_issue(const double* p, int64_t ld, bool kc, bool vec, int r0, int R, int k0, int Kd,
-                                           double* stage) {
+// Per-thread share of one operand's chunk copies: NP element pairs, each two
+// elements adjacent in memory, zero-filled outside the matrix.  VEC: one 16-byte
+// cp.async per pair (operand 16-byte aligned with an even ld), else two 8-byte
+// copies.  KC: the operand is contiguous along k (staged [row][k]), else along its
+// rows (staged [k][row]).  Per tile the pair's pointer and row validity are set;
+// per chunk the pointer advances by one chunk of k.  (With a zero source size
+// cp.async reads nothing, so the pointer may run past the matrix.)
+template <int BD, int NP, bool KC, bool VEC>
+struct GCopy {
+    const double* ptr[NP];    // element of the pair at the next chunk's k0
+    int lim[NP];              // KC: Kd - k if the row is inside, else 0;  !KC: Kd - k
+    int nrow[NP];             // !KC: elements of the pair inside along the rows (0..2)
+    static constexpr int NPAIR = GM_BKC * BD / 2;
+
+    __device__ __forceinline__ static int row_of(int pr) { return KC ? pr / (GM_BKC / 2) : 2 * (pr % (BD / 2)); }
+    __device__ __forceinline__ static int k_of(int pr) { return KC ? 2 * (pr % (GM_BKC / 2)) : pr / (BD / 2); }
+    __device__ __forceinline__ static int soff(int pr) {
+        return KC ? row_of(pr) * (GM_BKC + 4) + k_of(pr) : k_of(pr) * (BD + 4) + row_of(pr);
+    }
+    __device__ __forceinline__ void setup(const double* p, int64_t ld, int r0, int R, int Kd) {
 #pragma unroll
-    for (int e = 0; e < NP; ++e) {
-        const int pr = threadIdx.x + e * 256;
-        if (pr >= GM_BKC * BD / 2) break;
-        int r, k, so, n;   // n: valid elements of the pair
-        if (kc) {
-            k = 2 * (pr % (GM_BKC / 2)); r = pr / (GM_BKC / 2); so = r * (GM_BKC + 4) + k;
-            const int gk = k0 + k;
-            n = (r0 + r >= R) ? 0 : (gk + 1 < Kd ? 2 : (gk < Kd ? 1 : 0));
-        } else {
-            r = 2 * (pr % (BD / 2)); k = pr / (BD / 2); so = k * (BD + 4) + r;
-            const int gr = r0 + r;
-            n = (k0 + k >= Kd) ? 0 : (gr + 1 < R ? 2 : (gr < R ? 1 : 0));
-        }
-        const double* src = n ? p + (kc ? (int64_t)(r0 + r) * ld + (k0 + k) : (r0 + r) + (int64_t)(k0 + k) * ld) : p;
-        if (vec) {
-            cp_async16(stage + so, src, 8 * n);
-        } else {
-            cp_async8(stage + so, src, n >= 1);
-            cp_async8(stage + so + 1, n >= 2 ? src + 1 : p, n >= 2);
+        for (int e = 0; e < NP; ++e) {
+            const int pr = threadIdx.x + e * 256;
+            const int r = r0 + row_of(pr), k = k_of(pr);
+            ptr[e] = p + (KC ? (int64_t)r * ld + k : r + (int64_t)k * ld);
+            lim[e] = (KC && r >= R) ? 0 : Kd - k;
+            nrow[e] = KC ? 2 : (r + 1 < R ? 2 : (r < R ? 1 : 0));
         }
     }
-}
+    // copies the chunk at k0 (the chunks are issued in order) and advances
+    __device__ __forceinline__ void issue(int64_t ld, int k0, double* stage) {
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+            const int pr = threadIdx.x + e * 256;
+            if (NPAIR % 256 != 0 && pr >= NPAIR) break;
+            const int left = lim[e] - k0;
+            const int n = KC ? min(max(left, 0), 2) : (left > 0 ? nrow[e] : 0);
+            double* dst = stage + soff(pr);
+            if (VEC) {
+                cp_async16(dst, ptr[e], 8 * n);
+            } else {
+                cp_async8(dst, ptr[e], n >= 1);
+                cp_async8(dst + 1, ptr[e] + 1, n >= 2);
+            }
+            ptr[e] += KC ? (int64_t)GM_BKC : (int64_t)GM_BKC * ld;
+        }
+    }
+};
 
-template <int BM, int BN, int WM, int WN>
-__device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta, double* C,
-                         int64_t ldc, int first, int step, double* smem) {
+// TA / TB: op(A) = A^T / op(B) = B^T (compile time: the staged layouts and fragment
+// offsets become constants); the GOp's trans flags must agree (checked).
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, bool VA, bool VB>
+__device__ void cta_gemm_impl(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta, double* C,
+                              int64_t ldc, int first, int step, double* smem) {
     static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
     constexpr int FM = WM / 8, FN = WN / 8;              // DMMA blocks per warp
     constexpr int SA = gemm_stage_doubles<BM>(), SB = gemm_stage_doubles<BN>();   // doubles per stage
     constexpr int NPA = (GM_BKC * BM / 2 + 255) / 256, NPB = (GM_BKC * BN / 2 + 255) / 256;
+    // A^T is contiguous along k, A along rows; B along k, B^T along columns
+    constexpr bool KCA = TA, KCB = !TB;
+    // staged strides (doubles) of the tile row and of k for the fragment loads
+    constexpr int ARS = KCA ? GM_BKC + 4 : 1, AKS = KCA ? 1 : BM + 4;
+    constexpr int BRS = KCB ? GM_BKC + 4 : 1, BKS = KCB ? 1 : BN + 4;
     double* As = smem;                                   // [stage] A chunk
     double* Bs = smem + GM_NSC * SA;                     // [stage] B chunk
-    // A^T is contiguous along k, A along rows; B along k, B^T along columns
-    const bool kcA = A.trans, kcB = !B.trans;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
     const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
     const int nk = (Kd + GM_BKC - 1) / GM_BKC;
-    // staged strides (doubles) of the tile row and of k for the fragment loads
-    const int ars = kcA ? GM_BKC + 4 : 1, aks = kcA ? 1 : BM + 4;
-    const int brs = kcB ? GM_BKC + 4 : 1, bks = kcB ? 1 : BN + 4;
-    const int afo = t * aks + (wm + g) * ars, bfo = t * bks + (wn + g) * brs;
-    const bool vA = ((reinterpret_cast<uintptr_t>(A.p) & 15) == 0) && ((A.ld & 1) == 0);
-    const bool vB = ((reinterpret_cast<uintptr_t>(B.p) & 15) == 0) && ((B.ld & 1) == 0);
+    const int afo = t * AKS + (wm + g) * ARS, bfo = t * BKS + (wn + g) * BRS;
+    GCopy<BM, NPA, KCA, VA> ca;
+    GCopy<BN, NPB, KCB, VB> cb;
     for (int tile = first; tile < tm * tn; tile += step) {
         const int i0 = (tile % tm) * BM, j0 = (tile / tm) * BN;
+        ca.setup(A.p, A.ld, i0, M, Kd);
+        cb.setup(B.p, B.ld, j0, N, Kd);
         double acc[FM][FN][2];
 #pragma unroll
         for (int a = 0; a < FM; ++a)
@@ -132,8 +154,8 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
 #pragma unroll
         for (int s = 0; s < GM_NSC - 1; ++s) {
             if (s < nk) {
-                gemm_issue<BM, NPA>(A.p, A.ld, kcA, vA, i0, M, s * GM_BKC, Kd, As + s * SA);
-                gemm_issue<BN, NPB>(B.p, B.ld, kcB, vB, j0, N, s * GM_BKC, Kd, Bs + s * SB);
+                ca.issue(A.ld, s * GM_BKC, As + s * SA);
+                cb.issue(B.ld, s * GM_BKC, Bs + s * SB);
             }
             cp_async_commit();
         }
@@ -142,8 +164,8 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
             __syncthreads();
             if (kc + GM_NSC - 1 < nk) {
                 const int sn = (kc + GM_NSC - 1) % GM_NSC;
-                gemm_issue<BM, NPA>(A.p, A.ld, kcA, vA, i0, M, (kc + GM_NSC - 1) * GM_BKC, Kd, As + sn * SA);
-                gemm_issue<BN, NPB>(B.p, B.ld, kcB, vB, j0, N, (kc + GM_NSC - 1) * GM_BKC, Kd, Bs + sn * SB);
+                ca.issue(A.ld, (kc + GM_NSC - 1) * GM_BKC, As + sn * SA);
+                cb.issue(B.ld, (kc + GM_NSC - 1) * GM_BKC, Bs + sn * SB);
             }
             cp_async_commit();
             const double* as = As + (kc % GM_NSC) * SA + afo;
@@ -152,9 +174,9 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
             for (int kk = 0; kk < GM_BKC; kk += 4) {
                 double af[FM], bf[FN];
 #pragma unroll
-                for (int a = 0; a < FM; ++a) af[a] = as[kk * aks + a * 8 * ars];
+                for (int a = 0; a < FM; ++a) af[a] = as[kk * AKS + a * 8 * ARS];
 #pragma unroll
-                for (int b = 0; b < FN; ++b) bf[b] = bs[kk * bks + b * 8 * brs];
+                for (int b = 0; b < FN; ++b) bf[b] = bs[kk * BKS + b * 8 * BRS];
 #pragma unroll
                 for (int a = 0; a < FM; ++a)
 #pragma unroll
@@ -183,22 +205,34 @@ __device__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const 
     __syncthreads();
 }
 
-// the shapes used: wide 64 x 64 tiles, narrow 128 x 16 (tall probe blocks), short 16 x 128 (transposed probes)
+// 16-byte copies when both operands allow them (the planner's blocks and workspaces are
+// 16-byte aligned with even leading dimensions except for odd block sizes)
+template <int BM, int BN, int WM, int WN, bool TA, bool TB>
+__device__ __forceinline__ void cta_gemm(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta,
+                                         double* C, int64_t ldc, int first, int step, double* smem) {
+    if (A.trans != TA || B.trans != TB) __trap();
+    const bool vA = ((reinterpret_cast<uintptr_t>(A.p) & 15) == 0) && ((A.ld & 1) == 0);
+    const bool vB = ((reinterpret_cast<uintptr_t>(B.p) & 15) == 0) && ((B.ld & 1) == 0);
+    if (vA && vB) cta_gemm_impl<BM, BN, WM, WN, TA, TB, true, true>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
+    else cta_gemm_impl<BM, BN, WM, WN, TA, TB, false, false>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
+}
+
+// the shapes used: wide 64 x 64 tiles, narrow 128 x 16 (tall probe blocks), short 16 x 128
+// (transposed probes); the operand orientations are template arguments <TA, TB>
+template <bool TA, bool TB>
 __device__ __forceinline__ void gemm_wide(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta,
                                           double* C, int64_t ldc, int first, int step, double* smem) {
-    cta_gemm<64, 64, 16, 32>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
+    cta_gemm<64, 64, 16, 32, TA, TB>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
 }
+template <bool TA, bool TB>
 __device__ __forceinline__ void gemm_narrow(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta,
                                             double* C, int64_t ldc, int first, int step, double* smem) {
-    cta_gemm<128, 16, 16, 16>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
+    cta_gemm<128, 16, 16, 16, TA, TB>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
 }
-__device__ __forceinline__ void gemm_narrow64(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta,
-                                              double* C, int64_t ldc, int first, int step, double* smem) {
-    cta_gemm<64, 16, 8, 16>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
-}
+template <bool TA, bool TB>
 __device__ __forceinline__ void gemm_short(int M, int N, int Kd, double alpha, const GOp A, const GOp B, double beta,
                                            double* C, int64_t ldc, int first, int step, double* smem) {
-    cta_gemm<16, 128, 16, 16>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
+    cta_gemm<16, 128, 16, 16, TA, TB>(M, N, Kd, alpha, A, B, beta, C, ldc, first, step, smem);
 }
 __device__ __forceinline__ int gemm_tiles(int M, int N, int bm, int bn) { return ((M + bm - 1) / bm) * ((N + bn - 1) / bn); }
 

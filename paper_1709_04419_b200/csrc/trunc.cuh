@@ -377,7 +377,7 @@ __device__ __forceinline__ void gemm_tn_rsplit(int M, int N, int Kd, const doubl
         const int k0 = min(Kd, p * Kp), k1 = min(Kd, k0 + Kp);
         double* Cp = Rp + (int64_t)p * ldp * N;
         if (k1 > k0) {
-            gemm_wide(M, N, k1 - k0, 1.0, gop(A + k0, lda, true), gop(B + k0, ldb, false), 0.0, Cp, ldp, tile, tm * tn,
+            gemm_wide<true, false>(M, N, k1 - k0, 1.0, gop(A + k0, lda, true), gop(B + k0, ldb, false), 0.0, Cp, ldp, tile, tm * tn,
                       gsm);
         } else {
             const int i0 = (tile % tm) * 64, j0 = (tile / tm) * 64;
@@ -418,7 +418,7 @@ __device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int
     for (int c = sub; c < nchm; c += nsub) {
         const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
         // (128 x 16 tiles: one per 128 basis columns, not one per 16 of the 16 x 128 shape)
-        gemm_narrow(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
+        gemm_narrow<true, false>(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
                     gsm);
         first = false;
     }
@@ -435,7 +435,7 @@ __device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int
     __syncthreads();
     for (int c = sub; c < nchm; c += nsub) {
         const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        gemm_narrow(rows, nc, ell, -1.0, gop(W.Q + r0, m, false), gop(Cf, L, false), 1.0, X + r0, m, 0, 1, gsm);
+        gemm_narrow<false, false>(rows, nc, ell, -1.0, gop(W.Q + r0, m, false), gop(Cf, L, false), 1.0, X + r0, m, 0, 1, gsm);
     }
     // (no barrier: the partials are re-written only after the next coop_sync, and X's
     //  own rows are touched only by this CTA)
@@ -449,7 +449,7 @@ __device__ __forceinline__ void gram_owned(const TruncWs& W, int m, const double
     bool first = true;
     for (int c = sub; c < nchm; c += nsub) {
         const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        gemm_short(nc, nc, rows, 1.0, gop(X + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Gp, TR_RB, 0, 1,
+        gemm_short<true, false>(nc, nc, rows, 1.0, gop(X + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Gp, TR_RB, 0, 1,
                    gsm);
         first = false;
     }
@@ -658,7 +658,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
                                bar, gen, stt, gsm);
                 if (rowsplit) coop_sync(bar, nsub, gen, stt);   // the row-split R3 reads all of T
             } else {
-                gemm_wide(TR_PW, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_PW, sub, nsub, gsm);
+                gemm_wide<true, false>(TR_PW, K, q, 1.0, gop(W.Om, q, true), Vst, 0.0, W.Tt, TR_PW, sub, nsub, gsm);
                 coop_sync(bar, nsub, gen, stt);
             }
             // ---- R3: Y = U_stack T  (m x TR_PW), split over the stacked columns (each CTA one
@@ -668,14 +668,14 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             if (rowsplit) {
                 for (int c = sub; c < nchm; c += nsub) {
                     const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-                    gemm_wide(rows, TR_PW, K, 1.0, gop(W.Ast + r0, m, false), gop(W.Tt, TR_PW, true), 0.0, W.Y + r0, m,
+                    gemm_wide<false, true>(rows, TR_PW, K, 1.0, gop(W.Ast + r0, m, false), gop(W.Tt, TR_PW, true), 0.0, W.Y + r0, m,
                               0, 1, gsm);
                 }
                 __syncthreads();
             } else {
                 double* Yp = (nsub == 1) ? W.Y : W.Ypart + (int64_t)sub * m * TR_PW;
                 if (k1 > k0)
-                    gemm_wide(m, TR_PW, k1 - k0, 1.0, gop(W.Ast + (int64_t)k0 * m, m, false),
+                    gemm_wide<false, true>(m, TR_PW, k1 - k0, 1.0, gop(W.Ast + (int64_t)k0 * m, m, false),
                               gop(W.Tt + (int64_t)k0 * TR_PW, TR_PW, true), 0.0, Yp, m, 0, 1, gsm);
                 else
                     for (int idx = threadIdx.x; idx < m * TR_PW; idx += blockDim.x) Yp[idx] = 0.0;
@@ -857,7 +857,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
                        gsm);
         if (!(nsub > 1 && q <= TR_WSPLIT_Q)) coop_sync(bar, nsub, gen, stt);   // F2 below reads all of P
     } else {
-        gemm_wide(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
+        gemm_wide<true, false>(ell, K, m, 1.0, gop(W.Q, m, true), Ust, 0.0, W.Pt, L, sub, nsub, gsm);
         coop_sync(bar, nsub, gen, stt);
     }
     if (nsub > 1 && q <= TR_WSPLIT_Q) {            // split over the stacked columns, reduce owned rows
@@ -865,7 +865,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         const int k0 = min(K, sub * Kc), k1 = min(K, k0 + Kc);
         double* Wp = W.Wpart + (int64_t)sub * q * L;
         if (k1 > k0)
-            gemm_wide(q, ell, k1 - k0, 1.0, gop(W.Bst + (int64_t)k0 * q, q, false), gop(W.Pt + (int64_t)k0 * L, L, true),
+            gemm_wide<false, true>(q, ell, k1 - k0, 1.0, gop(W.Bst + (int64_t)k0 * q, q, false), gop(W.Pt + (int64_t)k0 * L, L, true),
                       0.0, Wp, q, 0, 1, gsm);
         else
             for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) Wp[idx] = 0.0;
@@ -880,7 +880,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             }
         }
     } else {
-        gemm_wide(q, ell, K, 1.0, Vst, gop(W.Pt, L, true), 0.0, W.Wm, q, sub, nsub, gsm);
+        gemm_wide<false, true>(q, ell, K, 1.0, Vst, gop(W.Pt, L, true), 0.0, W.Wm, q, sub, nsub, gsm);
     }
     coop_sync(bar, nsub, gen, stt);
     flops += 4.0 * (double)ell * K * (m + q);
@@ -896,7 +896,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         bool first = true;
         for (int c = sub; c < nchq; c += nsub) {
             const int r0 = c * TR_RCH, rows = min(q, r0 + TR_RCH) - r0;
-            gemm_wide(ell, ell, rows, 1.0, gop(W.Wm + r0, q, true), gop(W.Wm + r0, q, false), first ? 0.0 : 1.0, Gp, L, 0,
+            gemm_wide<true, false>(ell, ell, rows, 1.0, gop(W.Wm + r0, q, true), gop(W.Wm + r0, q, false), first ? 0.0 : 1.0, Gp, L, 0,
                       1, gsm);
             first = false;
         }
@@ -980,8 +980,8 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     if (r > 0) {
         // tiles of the V product start where the U tiles left off, so idle CTAs take them first
         const int tu = gemm_tiles(m, r, 64, 64);
-        gemm_wide(m, r, ell, 1.0, gop(W.Q, m, false), gop(W.Xo, L, false), 0.0, Uo, m, sub, nsub, gsm);
-        gemm_wide(q, r, ell, 1.0, gop(W.Wm, q, false), gop(W.G, L, false), 0.0, Vo, q, (sub + tu) % nsub, nsub, gsm);
+        gemm_wide<false, false>(m, r, ell, 1.0, gop(W.Q, m, false), gop(W.Xo, L, false), 0.0, Uo, m, sub, nsub, gsm);
+        gemm_wide<false, false>(q, r, ell, 1.0, gop(W.Wm, q, false), gop(W.G, L, false), 0.0, Vo, q, (sub + tu) % nsub, nsub, gsm);
     }
     if (sub == 0 && threadIdx.x == 0) {
         flops += 2.0 * (double)r * ell * (m + q);

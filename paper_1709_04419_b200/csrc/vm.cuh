@@ -22,6 +22,7 @@ struct TermRt {
     const double* b;
     int32_t lda, ldb, M, N, K, ch0;   // op(A) M x K, op(B) K x N; first chunk index
     int32_t ta, tb;
+    int32_t va, vb;                   // operand staged with 16-byte copies (contiguous along M / N, aligned)
     double alpha;
 };
 
@@ -31,7 +32,10 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
                                          const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by,
                                          double* dst = nullptr, int64_t ldd = 0, int drows = 0, int dcols = 0,
                                          double beta = 0.0, unsigned long long* stt = nullptr) {
-    constexpr int LA = 65, LB = 65, SA = GM_BK * LA, SB = GM_BK * LB;
+    // staged chunks [k][i] / [k][j]: ld 68 for an operand contiguous along the tile dimension
+    // (16-byte copies of element pairs, conflict-free fragment loads), 65 for one contiguous
+    // along k (8-byte copies; 65 keeps their stores conflict-free)
+    constexpr int SA = GM_BK * 68, SB = GM_BK * 68;
     __shared__ TermRt tr[VM_MAX_TERMS];
     __shared__ int s_nch;
     if (threadIdx.x < nt) {
@@ -50,6 +54,8 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         const int ka = v.ta ? ar : ac, kb = v.tb ? bc : br;
         r.K = ka < kb ? ka : kb;
         r.alpha = v.alpha;
+        r.va = !v.ta && ((reinterpret_cast<uintptr_t>(r.a) & 15) == 0) && ((v.a_ld & 1) == 0);
+        r.vb = v.tb && ((reinterpret_cast<uintptr_t>(r.b) & 15) == 0) && ((v.b_ld & 1) == 0);
         tr[threadIdx.x] = r;
     }
     __syncthreads();
@@ -85,19 +91,44 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         const int k0 = ik * GM_BK;
         double* as = As + (s % GM_NS) * SA;
         double* bs = Bs + (s % GM_NS) * SB;
+        if (r.va) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int idx = threadIdx.x + e * 256;     // 1024 = 64 x 16
-            int i, k;
-            if (r.ta) { k = idx % GM_BK; i = idx / GM_BK; } else { i = idx % 64; k = idx / 64; }
-            const bool ok = i < r.M && k0 + k < r.K;
-            cp_async8(as + k * LA + i, ok ? (r.ta ? r.a + (k0 + k) + (int64_t)i * r.lda : r.a + i + (int64_t)(k0 + k) * r.lda) : r.a,
-                      ok);
-            int j, kb;
-            if (r.tb) { j = idx % 64; kb = idx / 64; } else { kb = idx % GM_BK; j = idx / GM_BK; }
-            const bool okb = j < r.N && k0 + kb < r.K;
-            cp_async8(bs + kb * LB + j,
-                      okb ? (r.tb ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b + (k0 + kb) + (int64_t)j * r.ldb) : r.b, okb);
+            for (int e = 0; e < 2; ++e) {                // 512 pairs = 64 x 16 / 2
+                const int pr = threadIdx.x + e * 256, i = 2 * (pr & 31), k = pr >> 5;
+                const int n = (k0 + k < r.K) ? (i + 1 < r.M ? 2 : (i < r.M ? 1 : 0)) : 0;
+                cp_async16(as + k * 68 + i, n ? r.a + i + (int64_t)(k0 + k) * r.lda : r.a, 8 * n);
+            }
+        } else {
+            const int la = r.ta ? 65 : 68;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int idx = threadIdx.x + e * 256;     // 1024 = 64 x 16
+                int i, k;
+                if (r.ta) { k = idx % GM_BK; i = idx / GM_BK; } else { i = idx % 64; k = idx / 64; }
+                const bool ok = i < r.M && k0 + k < r.K;
+                cp_async8(as + k * la + i,
+                          ok ? (r.ta ? r.a + (k0 + k) + (int64_t)i * r.lda : r.a + i + (int64_t)(k0 + k) * r.lda) : r.a, ok);
+            }
+        }
+        if (r.vb) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int pr = threadIdx.x + e * 256, j = 2 * (pr & 31), kb = pr >> 5;
+                const int n = (k0 + kb < r.K) ? (j + 1 < r.N ? 2 : (j < r.N ? 1 : 0)) : 0;
+                cp_async16(bs + kb * 68 + j, n ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b, 8 * n);
+            }
+        } else {
+            const int lb = r.tb ? 68 : 65;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int idx = threadIdx.x + e * 256;
+                int j, kb;
+                if (r.tb) { j = idx % 64; kb = idx / 64; } else { kb = idx % GM_BK; j = idx / GM_BK; }
+                const bool okb = j < r.N && k0 + kb < r.K;
+                cp_async8(bs + kb * lb + j,
+                          okb ? (r.tb ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b + (k0 + kb) + (int64_t)j * r.ldb) : r.b,
+                          okb);
+            }
         }
         ++ik;
     };
@@ -105,6 +136,7 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
     auto compute = [&](int s) {
         while (ct < nt && ck >= (tr[ct].K + GM_BK - 1) / GM_BK) { ++ct; ck = 0; }
         const double al = tr[ct].alpha;
+        const int la = tr[ct].ta ? 65 : 68, lb = tr[ct].tb ? 68 : 65;
         // fragments outside this term's op(A) rows / op(B) columns get zeros from it: skip
         // their DMMAs (warp-uniform; low-rank factors are often much narrower than 64)
         const int am = tr[ct].M - wm, bn = tr[ct].N - wn, kr = tr[ct].K - ck * GM_BK;
@@ -117,9 +149,9 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
             if (kk >= kr) break;
             double af[2], bf[4];
 #pragma unroll
-            for (int a = 0; a < 2; ++a) af[a] = al * as[(kk + t4) * LA + wm + a * 8 + g];
+            for (int a = 0; a < 2; ++a) af[a] = al * as[(kk + t4) * la + wm + a * 8 + g];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) bf[b] = bs[(kk + t4) * LB + wn + b * 8 + g];
+            for (int b = 0; b < 4; ++b) bf[b] = bs[(kk + t4) * lb + wn + b * 8 + g];
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll

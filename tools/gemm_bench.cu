@@ -8,15 +8,22 @@
 #include "../paper_1709_04419_b200/csrc/gemm.cuh"
 using namespace hm;
 
+template <int SHAPE, bool TA, bool TB>
+__device__ void gemm_shape(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                           double* sm) {
+    if (SHAPE == 0) gemm_wide<TA, TB>(M, N, K, 1.0, gop(A, lda, TA), gop(B, ldb, TB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
+    if (SHAPE == 1) gemm_narrow<TA, TB>(M, N, K, 1.0, gop(A, lda, TA), gop(B, ldb, TB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
+    if (SHAPE == 2) gemm_short<TA, TB>(M, N, K, 1.0, gop(A, lda, TA), gop(B, ldb, TB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
+}
 template <int SHAPE>
 __global__ void kgemm(int M, int N, int K, const double* A, int lda, bool tA, const double* B, int ldb, bool tB,
                       double* C, int ldc, int reps) {
     extern __shared__ double sm[];
     for (int r = 0; r < reps; ++r) {
-        if (SHAPE == 0) gemm_wide(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
-        if (SHAPE == 1) gemm_narrow(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
-        if (SHAPE == 2) gemm_short(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
-        if (SHAPE == 3) gemm_narrow64(M, N, K, 1.0, gop(A, lda, tA), gop(B, ldb, tB), 0.0, C, ldc, blockIdx.x, gridDim.x, sm);
+        if (tA && tB) gemm_shape<SHAPE, true, true>(M, N, K, A, lda, B, ldb, C, ldc, sm);
+        if (tA && !tB) gemm_shape<SHAPE, true, false>(M, N, K, A, lda, B, ldb, C, ldc, sm);
+        if (!tA && tB) gemm_shape<SHAPE, false, true>(M, N, K, A, lda, B, ldb, C, ldc, sm);
+        if (!tA && !tB) gemm_shape<SHAPE, false, false>(M, N, K, A, lda, B, ldb, C, ldc, sm);
     }
 }
 __global__ void kref(int M, int N, int K, const double* A, int lda, bool tA, const double* B, int ldb, bool tB, double* C,
@@ -60,7 +67,6 @@ void run(const char* name, int M, int N, int K, bool tA, bool tB, int grid) {
 }
 int main() {
     run<1>("narrow", 256, 16, 1700, false, true, 1);      // R3: Y = Ast T
-    run<3>("narrow64", 128, 16, 1500, false, true, 1);    // R3 small
     run<2>("short", 16, 1500, 128, true, false, 1);       // R2 small
     run<2>("short", 16, 1700, 256, true, false, 1);       // R2: T^T = Om^T Bst
     run<0>("wide", 48, 1700, 256, true, false, 1);        // F1: P^T = Q^T Ast
