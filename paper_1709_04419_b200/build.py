@@ -48,6 +48,14 @@ def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     objs, log = [], []
+    # a change of HM_BUILD_DEFS rebuilds everything
+    stamp = os.path.join(OBJ, "defs.txt")
+    defs = " ".join(EXTRA)
+    if not os.path.exists(stamp) or open(stamp).read() != defs:
+        for o in glob.glob(os.path.join(OBJ, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as f:
+            f.write(defs)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
         if _newer(src, obj):

@@ -409,20 +409,24 @@ __device__ __forceinline__ int piece_of(const int* koff, int np, int k) {
 
 
 
-// X[:, 0:nc] <- X - Q[:, 0:ell] (Q^T X) on this CTA's own row chunks; the ell x nc
+// Row ownership in a cooperative truncation: CTA sub owns the contiguous 64-row
+// chunks [nch sub / nsub, nch (sub + 1) / nsub), so each of its row-local products
+// is one GEMM call (one pipeline) instead of one per chunk.
+__device__ __forceinline__ void own_rows(int len, int sub, int nsub, int& r0, int& r1) {
+    const int nch = (len + TR_RCH - 1) / TR_RCH;
+    r0 = min(len, (int)((int64_t)nch * sub / nsub) * TR_RCH);
+    r1 = min(len, (int)((int64_t)nch * (sub + 1) / nsub) * TR_RCH);
+}
+
+// X[:, 0:nc] <- X - Q[:, 0:ell] (Q^T X) on this CTA's own rows [r0, r1); the ell x nc
 // product is reduced over the group through per-CTA partials (one barrier).
 __device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int L, double* X, int nc, int sub, int nsub,
-                                           int nchm, int* bar, int& gen, unsigned long long* stt, double* gsm) {
+                                           int r0, int r1, int* bar, int& gen, unsigned long long* stt, double* gsm) {
     double* Cp = W.Cp + (int64_t)sub * L * TR_RB;
-    bool first = true;
-    for (int c = sub; c < nchm; c += nsub) {
-        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        // (128 x 16 tiles: one per 128 basis columns, not one per 16 of the 16 x 128 shape)
-        gemm_narrow<true, false>(ell, nc, rows, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Cp, L, 0, 1,
-                    gsm);
-        first = false;
-    }
-    if (first)
+    if (r1 > r0)
+        gemm_narrow<true, false>(ell, nc, r1 - r0, 1.0, gop(W.Q + r0, m, true), gop(X + r0, m, false), 0.0, Cp, L, 0, 1,
+                                 gsm);
+    else
         for (int idx = threadIdx.x; idx < ell * nc; idx += blockDim.x) Cp[(idx % ell) + (int64_t)(idx / ell) * L] = 0.0;
     coop_sync(bar, nsub, gen, stt);
     double* Cf = W.Cf + (int64_t)sub * L * TR_RB;
@@ -433,27 +437,22 @@ __device__ __forceinline__ void proj_owned(const TruncWs& W, int m, int ell, int
         Cf[e] = a;
     }
     __syncthreads();
-    for (int c = sub; c < nchm; c += nsub) {
-        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        gemm_narrow<false, false>(rows, nc, ell, -1.0, gop(W.Q + r0, m, false), gop(Cf, L, false), 1.0, X + r0, m, 0, 1, gsm);
-    }
+    if (r1 > r0)
+        gemm_narrow<false, false>(r1 - r0, nc, ell, -1.0, gop(W.Q + r0, m, false), gop(Cf, L, false), 1.0, X + r0, m, 0,
+                                  1, gsm);
     // (no barrier: the partials are re-written only after the next coop_sync, and X's
     //  own rows are touched only by this CTA)
 }
 
 // Gs (shared, nc x nc, ld TR_RB) = X[:, 0:nc]^T X[:, 0:nc], reduced over the group
-__device__ __forceinline__ void gram_owned(const TruncWs& W, int m, const double* X, int nc, int sub, int nsub,
-                                           int nchm, int* bar, int& gen, unsigned long long* stt, double* gsm,
+__device__ __forceinline__ void gram_owned(const TruncWs& W, int m, const double* X, int nc, int sub, int nsub, int r0,
+                                           int r1, int* bar, int& gen, unsigned long long* stt, double* gsm,
                                            double* Gs) {
     double* Gp = W.Gp + (int64_t)sub * TR_RB * TR_RB;
-    bool first = true;
-    for (int c = sub; c < nchm; c += nsub) {
-        const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-        gemm_short<true, false>(nc, nc, rows, 1.0, gop(X + r0, m, true), gop(X + r0, m, false), first ? 0.0 : 1.0, Gp, TR_RB, 0, 1,
-                   gsm);
-        first = false;
-    }
-    if (first)
+    if (r1 > r0)
+        gemm_short<true, false>(nc, nc, r1 - r0, 1.0, gop(X + r0, m, true), gop(X + r0, m, false), 0.0, Gp, TR_RB, 0, 1,
+                                gsm);
+    else
         for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) Gp[(idx % nc) + (idx / nc) * TR_RB] = 0.0;
     coop_sync(bar, nsub, gen, stt);
     for (int idx = threadIdx.x; idx < TR_RB * TR_RB; idx += blockDim.x) {
@@ -565,6 +564,9 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     const bool rowsplit = nsub > 1 && (m + TR_RCH - 1) / TR_RCH >= nsub;   // R3 over owned rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nchm = (m + TR_RCH - 1) / TR_RCH, nchq = (q + TR_RCH - 1) / TR_RCH;
+    int om0, om1, oq0, oq1;                        // this CTA's own rows of the m- and q-sides
+    own_rows(m, sub, nsub, om0, om1);
+    own_rows(q, sub, nsub, oq0, oq1);
     TruncWs W = trunc_ws_layout(pool + t.ws, m, q, cap, Ks, t.nsub);
     int* ctl = (int*)W.ctl;                        // [0] done, [1] ell, [2] rank, [3] added, [8..] order
     double* gsm = dsm;                             // GEMM staging
@@ -666,11 +668,9 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             // (tall blocks, at least one 64-row chunk per CTA: split over the owned row chunks
             // instead -- no partial sums)
             if (rowsplit) {
-                for (int c = sub; c < nchm; c += nsub) {
-                    const int r0 = c * TR_RCH, rows = min(m, r0 + TR_RCH) - r0;
-                    gemm_wide<false, true>(rows, TR_PW, K, 1.0, gop(W.Ast + r0, m, false), gop(W.Tt, TR_PW, true), 0.0, W.Y + r0, m,
-                              0, 1, gsm);
-                }
+                if (om1 > om0)
+                    gemm_wide<false, true>(om1 - om0, TR_PW, K, 1.0, gop(W.Ast + om0, m, false), gop(W.Tt, TR_PW, true), 0.0,
+                                           W.Y + om0, m, 0, 1, gsm);
                 __syncthreads();
             } else {
                 double* Yp = (nsub == 1) ? W.Y : W.Ypart + (int64_t)sub * m * TR_PW;
@@ -684,7 +684,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         }
         flops += 4.0 * TR_PW * (double)K * (m + q);
         bytes += 8.0 * Srows;
-        for (int c = sub; c < nchm; c += nsub) {
+        for (int c = om0 / TR_RCH; c * TR_RCH < om1; ++c) {
             const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
             if (nsub > 1 && !rowsplit) {
                 for (int idx = threadIdx.x; idx < (r1 - r0) * TR_PW; idx += blockDim.x) {
@@ -722,10 +722,10 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         // Partial reductions over each CTA's own 64-row chunks are summed by every CTA
         // in the same order, so all CTAs take the same decisions without a broadcast.
         if (ell > 0) {
-            for (int pass = 0; pass < 2; ++pass) proj_owned(W, m, ell, L, Yb, TR_RB, sub, nsub, nchm, bar, gen, stt, gsm);
+            for (int pass = 0; pass < 2; ++pass) proj_owned(W, m, ell, L, Yb, TR_RB, sub, nsub, om0, om1, bar, gen, stt, gsm);
             flops += 8.0 * TR_RB * (double)ell * m;
         }
-        gram_owned(W, m, Yb, TR_RB, sub, nsub, nchm, bar, gen, stt, gsm, Gs);
+        gram_owned(W, m, Yb, TR_RB, sub, nsub, om0, om1, bar, gen, stt, gsm, Gs);
         // pivoted Cholesky (redundant, identical in every CTA): accept pivots above
         // max(thr, 1e-4 * largest) so R stays well conditioned (cond <= 1e4); weaker
         // directions are picked up by the next round's probes
@@ -776,8 +776,8 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         const double maxn = s_maxn;
         if (na > 0) {
             // Qn = Y_P R^-1 on the owned rows (thread per row, forward substitution)
-            for (int c = sub; c < nchm; c += nsub) {
-                const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+            {
+                const int r0 = om0, r1 = om1;
                 for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
                     double x[TR_RB];
 #pragma unroll
@@ -793,8 +793,8 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             }
             __syncthreads();
             double* Qn = W.Q + (int64_t)ell * m;
-            if (ell > 0) proj_owned(W, m, ell, L, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm);
-            gram_owned(W, m, Qn, na, sub, nsub, nchm, bar, gen, stt, gsm, Gs);
+            if (ell > 0) proj_owned(W, m, ell, L, Qn, na, sub, nsub, om0, om1, bar, gen, stt, gsm);
+            gram_owned(W, m, Qn, na, sub, nsub, om0, om1, bar, gen, stt, gsm, Gs);
             // CholQR of the (nearly orthonormal) new block: Qn <- Qn chol(Qn^T Qn)^-1
             // (warp 0: lane j forms row k's entry j; sums in the order l = 0 .. k-1)
             if (warp == 0) {
@@ -811,8 +811,8 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
                 }
             }
             __syncthreads();
-            for (int c = sub; c < nchm; c += nsub) {
-                const int r0 = c * TR_RCH, r1 = min(m, r0 + TR_RCH);
+            {
+                const int r0 = om0, r1 = om1;
                 for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
                     double x[TR_RB];
 #pragma unroll
@@ -893,14 +893,10 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
         // rank-revealing factorisation, resolving sigma_i / sigma_1 down to ~1e-8 -- enough
         // for eps >= 1e-7 -- at a fraction of the cost of an iterative eigensolver.
         double* Gp = W.Gp2 + (int64_t)sub * L * L;
-        bool first = true;
-        for (int c = sub; c < nchq; c += nsub) {
-            const int r0 = c * TR_RCH, rows = min(q, r0 + TR_RCH) - r0;
-            gemm_wide<true, false>(ell, ell, rows, 1.0, gop(W.Wm + r0, q, true), gop(W.Wm + r0, q, false), first ? 0.0 : 1.0, Gp, L, 0,
-                      1, gsm);
-            first = false;
-        }
-        if (first)
+        if (oq1 > oq0)
+            gemm_wide<true, false>(ell, ell, oq1 - oq0, 1.0, gop(W.Wm + oq0, q, true), gop(W.Wm + oq0, q, false), 0.0, Gp,
+                                   L, 0, 1, gsm);
+        else
             for (int idx = threadIdx.x; idx < ell * ell; idx += blockDim.x) Gp[(idx % ell) + (int64_t)(idx / ell) * L] = 0.0;
         coop_sync(bar, nsub, gen, stt);
         for (int idx = sub * blockDim.x + threadIdx.x; idx < ell * ell; idx += nsub * blockDim.x) {

@@ -20,3 +20,6 @@ T = hm.Tree(pts, leaf, 2.0)
 T.plan_dump(f"/tmp/plan_{which}.bin", KMAX)
 print(H.timings())
 print(analyse(f"/tmp/plan_{which}.bin", f"/tmp/trace_{which}.bin", "chol", grid=148))
+import subprocess
+print(subprocess.run([sys.executable, "/root/repo/tools/stall_probe.py", f"/tmp/plan_{which}.bin", f"/tmp/trace_{which}.bin"],
+                     capture_output=True, text=True).stdout)
