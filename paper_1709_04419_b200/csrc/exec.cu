@@ -23,7 +23,7 @@
 
 namespace hm {
 
-constexpr int EXEC_SMEM = (NTILE * TSZ * 8 > TR_SMEM) ? NTILE * TSZ * 8 : TR_SMEM;
+constexpr int EXEC_SMEM = (VM_SMEM > TR_SMEM) ? VM_SMEM : TR_SMEM;
 
 
 __global__ void __launch_bounds__(TTHREADS, 2)

@@ -223,12 +223,12 @@ void launch_aca(const AcaTask* t, int n, const double* pts, double* pool, int* r
 void vm_set_attr() {
     static bool done = false;
     if (done) return;
-    HM_CUDA_TRY(cudaFuncSetAttribute(k_vm, cudaFuncAttributeMaxDynamicSharedMemorySize, NTILE * TSZ * 8));
+    HM_CUDA_TRY(cudaFuncSetAttribute(k_vm, cudaFuncAttributeMaxDynamicSharedMemorySize, VM_SMEM));
     done = true;
 }
 void launch_vm(const VTask* t, int n, const VIns* ins, const VTerm* terms, double* pool, const int* ranks, int* flags,
                double* ctr, cudaStream_t st) {
-    if (n > 0) k_vm<<<n, TTHREADS, NTILE * TSZ * 8, st>>>(t, ins, terms, pool, ranks, flags, ctr);
+    if (n > 0) k_vm<<<n, TTHREADS, VM_SMEM, st>>>(t, ins, terms, pool, ranks, flags, ctr);
 }
 void launch_gather(const double* Z, const int64_t* perm, int64_t n, int kz, int zw, double* Zt, cudaStream_t st) {
     const int64_t tot = n * zw;

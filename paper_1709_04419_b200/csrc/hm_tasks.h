@@ -127,6 +127,13 @@ constexpr int64_t TR_COOP_WORK = int64_t(1) << HM_COOP_WORK_LOG2;   // (m + q) *
 constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation (hard limit; the plan's
                                   // cap hm_params.coop_max defaults to TR_COOP_DEFAULT)
 constexpr int TR_COOP_DEFAULT = 16;
+#ifndef HM_TR_SHRINK
+#define HM_TR_SHRINK 1
+#endif
+constexpr int TR_SHRINK = HM_TR_SHRINK;   // > 0: a cooperative truncation keeps one CTA per TR_SHRINK
+                                          // 64-row chunks after its first probe pass (trunc.cuh);
+                                          // measured at n = 64k, S = 4: 1 -> 6.84 evals/s, 2 -> 6.60,
+                                          // 0 (off) -> 6.62 (one evaluation 397 / 464 / 383 ms)
 
 struct TruncWs {                  // randomized-path workspace (doubles unless noted)
     double *ctl, *Om, *Ast, *Bst, *Tt, *Y, *npart, *Q, *Cb, *Pt, *Wm, *Wc, *S, *Z, *Xo, *G, *tau, *sig, *Cp, *Cf, *Gp,

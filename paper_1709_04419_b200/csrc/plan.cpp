@@ -1090,7 +1090,11 @@ struct Builder {
         t.eps_scale = eps_scale;
         if ((int32_t)pcs.size() > TR_PMAX) throw std::logic_error("truncation with more than TR_PMAX pieces");
         t.nsub = nsub;
-        t.bar = t.nsub > 1 ? ph->n_bars++ : 0;
+        t.bar = 0;
+        if (t.nsub > 1) {                                 // two counters: the group, then its shrunk core
+            t.bar = ph->n_bars;
+            ph->n_bars += 2;
+        }
         ph->tp.insert(ph->tp.end(), pcs.begin(), pcs.end());
         xraw.push_back({w, 1, (int32_t)traw.size(), std::move(deps)});
         traw.push_back({w, t});

@@ -557,11 +557,12 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
                                   int* __restrict__ ranks, int* __restrict__ flags, double eps,
                                   double* __restrict__ ctr, double* dsm, int sub, int nsub, int* bar,
                                   unsigned long long* stt) {
+    // (nsub, bar: the group may shrink after the first round's probes, see below)
     const int m = t.m, q = t.q, cap = t.cap, np = t.piece_count;
     const int L = cap + TR_RB;
     const int Ks = t.kmax_tot;
-    const int rsplit = (nsub == t.nsub) ? trunc_rsplit(m, q, cap, Ks, t.nsub) : 1;
-    const bool rowsplit = nsub > 1 && (m + TR_RCH - 1) / TR_RCH >= nsub;   // R3 over owned rows
+    int rsplit = (nsub == t.nsub) ? trunc_rsplit(m, q, cap, Ks, t.nsub) : 1;
+    bool rowsplit = nsub > 1 && (m + TR_RCH - 1) / TR_RCH >= nsub;   // R3 over owned rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nchm = (m + TR_RCH - 1) / TR_RCH, nchq = (q + TR_RCH - 1) / TR_RCH;
     int om0, om1, oq0, oq1;                        // this CTA's own rows of the m- and q-sides
@@ -703,6 +704,24 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             }
         }
         coop_sync(bar, nsub, gen, stt);
+        // ---- shrink (first round): the row-owned middle (BCGS2) and the final products run
+        // on nkeep CTAs (HM_TR_SHRINK 64-row chunks each); the others leave for other tasks
+        // instead of waiting at the group's barriers.  A fresh barrier counter (bar + 1) takes over:
+        // each kept CTA credits it with gen arrivals, so the generation count (and the stage
+        // stamps) simply continue; partial buffers are indexed by sub < nkeep.
+        if (TR_SHRINK > 0 && round == 0) {
+            const int nkeep = min(nsub, (nchm + TR_SHRINK - 1) / TR_SHRINK);
+            if (nkeep < nsub) {
+                if (sub >= nkeep) return;
+                nsub = nkeep;
+                bar += 1;
+                if (threadIdx.x == 0) atomicAdd(bar, gen);
+                rsplit = 1;
+                rowsplit = nsub > 1 && nchm >= nsub;
+                own_rows(m, sub, nsub, om0, om1);
+                own_rows(q, sub, nsub, oq0, oq1);
+            }
+        }
         // ---- scale: max_j ||M w_j|| over the probes seen so far (every CTA, same order)
         if (threadIdx.x < TR_PW) {
             const int j = threadIdx.x;

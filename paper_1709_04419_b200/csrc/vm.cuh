@@ -14,17 +14,56 @@ namespace hm {
 
 // VM_MGEMM: T0 (64 x 64 smem tile) += sum_t alpha_t op(A_t) op(B_t).  The (term, 16-wide
 // K chunk) sequence of all terms is streamed global -> shared memory through a
-// GM_NS-stage cp.async pipeline (zero-filled outside each operand's dims) into
-// `stage` (the free tiles 1..2), and accumulated in registers by the FP64 tensor
+// VM_NS-stage cp.async pipeline (zero-filled outside each operand's dims) into
+// the staging area behind the NTILE tiles (VM_SMEM), and accumulated in registers by the FP64 tensor
 // cores (warp tile 16 x 32, 4 x 2 warps); T0 is updated once at the end.
 struct TermRt {
     const double* a;
     const double* b;
     int32_t lda, ldb, M, N, K, ch0;   // op(A) M x K, op(B) K x N; first chunk index
     int32_t ta, tb;
-    int32_t va, vb;                   // operand staged with 16-byte copies (contiguous along M / N, aligned)
+    int32_t va, vb;                   // operand staged with 16-byte copies (aligned, even ld)
     double alpha;
 };
+
+// One operand's K chunk (rows [0, R) x k in [k0, k0 + GM_BK) of op(X), K columns in all)
+// into a stage: kc = contiguous along k (X^T of a column-major A, or B), staged [row][k]
+// with ld 20, else [k][row] with ld 68; vec = 16-byte element pairs along the contiguous
+// dimension, else 8-byte copies; zero-filled outside the operand.
+constexpr int VM_NS = 4;                         // pipeline stages
+constexpr int VM_STAGE = 64 * 20;                // doubles per stage (>= GM_BK * 68)
+static_assert(GM_BK * 68 <= VM_STAGE, "stage holds either layout");
+constexpr int VM_SMEM = (NTILE * TSZ + 2 * VM_NS * VM_STAGE) * 8;   // bytes: tiles + A / B stages
+__device__ __forceinline__ void vm_stage(double* st, const double* p, int64_t ld, bool kc, bool vec, int R, int K,
+                                         int k0) {
+    if (vec) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {                    // 512 pairs = 64 x 16 / 2
+            const int pr = threadIdx.x + e * 256;
+            int r, k, so, n;
+            if (kc) {
+                k = 2 * (pr & 7); r = pr >> 3; so = r * 20 + k;
+                const int left = K - k0 - k;
+                n = (r < R) ? (left >= 2 ? 2 : (left > 0 ? left : 0)) : 0;
+            } else {
+                r = 2 * (pr & 31); k = pr >> 5; so = k * 68 + r;
+                n = (k0 + k < K) ? (r + 1 < R ? 2 : (r < R ? 1 : 0)) : 0;
+            }
+            const double* src = kc ? p + (k0 + k) + (int64_t)r * ld : p + r + (int64_t)(k0 + k) * ld;
+            cp_async16(st + so, n ? src : p, 8 * n);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = threadIdx.x + e * 256;       // 1024 = 64 x 16
+            int r, k, so;
+            if (kc) { k = idx & 15; r = idx >> 4; so = r * 20 + k; }
+            else { r = idx & 63; k = idx >> 6; so = k * 68 + r; }
+            const bool ok = r < R && k0 + k < K;
+            cp_async8(st + so, ok ? (kc ? p + (k0 + k) + (int64_t)r * ld : p + r + (int64_t)(k0 + k) * ld) : p, ok);
+        }
+    }
+}
 
 // dst == nullptr: T0 += result (smem tile); else dst[r + c ldd] = beta dst + result for
 // r < drows, c < dcols (VM_MGEMM_ST: accumulators straight to global memory)
@@ -32,10 +71,11 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
                                          const int* ranks, double* stageA, double* stageB, double& c_fl, double& c_by,
                                          double* dst = nullptr, int64_t ldd = 0, int drows = 0, int dcols = 0,
                                          double beta = 0.0, unsigned long long* stt = nullptr) {
-    // staged chunks [k][i] / [k][j]: ld 68 for an operand contiguous along the tile dimension
-    // (16-byte copies of element pairs, conflict-free fragment loads), 65 for one contiguous
-    // along k (8-byte copies; 65 keeps their stores conflict-free)
-    constexpr int SA = GM_BK * 68, SB = GM_BK * 68;
+    // staged chunks: an operand contiguous along the tile dimension (A, B^T) as [k][row]
+    // with ld 68, one contiguous along k (A^T, B) as [row][k] with ld 20 -- both keep rows
+    // 16-byte aligned for 16-byte copies of element pairs and make the fragment loads
+    // conflict-free (bank offsets 8t + 2g resp. 8g + 2t per half-warp)
+    constexpr int SA = VM_STAGE, SB = VM_STAGE;
     __shared__ TermRt tr[VM_MAX_TERMS];
     __shared__ int s_nch;
     if (threadIdx.x < nt) {
@@ -54,8 +94,8 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         const int ka = v.ta ? ar : ac, kb = v.tb ? bc : br;
         r.K = ka < kb ? ka : kb;
         r.alpha = v.alpha;
-        r.va = !v.ta && ((reinterpret_cast<uintptr_t>(r.a) & 15) == 0) && ((v.a_ld & 1) == 0);
-        r.vb = v.tb && ((reinterpret_cast<uintptr_t>(r.b) & 15) == 0) && ((v.b_ld & 1) == 0);
+        r.va = ((reinterpret_cast<uintptr_t>(r.a) & 15) == 0) && ((v.a_ld & 1) == 0);
+        r.vb = ((reinterpret_cast<uintptr_t>(r.b) & 15) == 0) && ((v.b_ld & 1) == 0);
         tr[threadIdx.x] = r;
     }
     __syncthreads();
@@ -72,8 +112,7 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
     }
     __syncthreads();
     const int nch = s_nch;
-    static_assert(GM_NS * SA <= TSZ && GM_NS * SB <= TSZ, "stages fit one tile each");
-    double* As = stageA;                                 // the two tiles other than T0
+    double* As = stageA;                                 // VM_NS stages each (exec.cu: behind the tiles)
     double* Bs = stageB;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
@@ -89,69 +128,32 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         while (it < nt && ik >= (tr[it].K + GM_BK - 1) / GM_BK) { ++it; ik = 0; }
         const TermRt r = tr[it];
         const int k0 = ik * GM_BK;
-        double* as = As + (s % GM_NS) * SA;
-        double* bs = Bs + (s % GM_NS) * SB;
-        if (r.va) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {                // 512 pairs = 64 x 16 / 2
-                const int pr = threadIdx.x + e * 256, i = 2 * (pr & 31), k = pr >> 5;
-                const int n = (k0 + k < r.K) ? (i + 1 < r.M ? 2 : (i < r.M ? 1 : 0)) : 0;
-                cp_async16(as + k * 68 + i, n ? r.a + i + (int64_t)(k0 + k) * r.lda : r.a, 8 * n);
-            }
-        } else {
-            const int la = r.ta ? 65 : 68;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int idx = threadIdx.x + e * 256;     // 1024 = 64 x 16
-                int i, k;
-                if (r.ta) { k = idx % GM_BK; i = idx / GM_BK; } else { i = idx % 64; k = idx / 64; }
-                const bool ok = i < r.M && k0 + k < r.K;
-                cp_async8(as + k * la + i,
-                          ok ? (r.ta ? r.a + (k0 + k) + (int64_t)i * r.lda : r.a + i + (int64_t)(k0 + k) * r.lda) : r.a, ok);
-            }
-        }
-        if (r.vb) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int pr = threadIdx.x + e * 256, j = 2 * (pr & 31), kb = pr >> 5;
-                const int n = (k0 + kb < r.K) ? (j + 1 < r.N ? 2 : (j < r.N ? 1 : 0)) : 0;
-                cp_async16(bs + kb * 68 + j, n ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b, 8 * n);
-            }
-        } else {
-            const int lb = r.tb ? 68 : 65;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int idx = threadIdx.x + e * 256;
-                int j, kb;
-                if (r.tb) { j = idx % 64; kb = idx / 64; } else { kb = idx % GM_BK; j = idx / GM_BK; }
-                const bool okb = j < r.N && k0 + kb < r.K;
-                cp_async8(bs + kb * lb + j,
-                          okb ? (r.tb ? r.b + j + (int64_t)(k0 + kb) * r.ldb : r.b + (k0 + kb) + (int64_t)j * r.ldb) : r.b,
-                          okb);
-            }
-        }
+        double* as = As + (s % VM_NS) * SA;
+        double* bs = Bs + (s % VM_NS) * SB;
+        vm_stage(as, r.a, r.lda, r.ta != 0, r.va != 0, r.M, r.K, k0);
+        vm_stage(bs, r.b, r.ldb, r.tb == 0, r.vb != 0, r.N, r.K, k0);
         ++ik;
     };
     int ct = 0, ck = 0;                                  // compute cursor
     auto compute = [&](int s) {
         while (ct < nt && ck >= (tr[ct].K + GM_BK - 1) / GM_BK) { ++ct; ck = 0; }
         const double al = tr[ct].alpha;
-        const int la = tr[ct].ta ? 65 : 68, lb = tr[ct].tb ? 68 : 65;
+        const bool kcA = tr[ct].ta != 0, kcB = tr[ct].tb == 0;
         // fragments outside this term's op(A) rows / op(B) columns get zeros from it: skip
         // their DMMAs (warp-uniform; low-rank factors are often much narrower than 64)
         const int am = tr[ct].M - wm, bn = tr[ct].N - wn, kr = tr[ct].K - ck * GM_BK;
         ++ck;
         if (am <= 0 || bn <= 0) return;
-        const double* as = As + (s % GM_NS) * SA;
-        const double* bs = Bs + (s % GM_NS) * SB;
+        const double* as = As + (s % VM_NS) * SA;
+        const double* bs = Bs + (s % VM_NS) * SB;
 #pragma unroll
         for (int kk = 0; kk < GM_BK; kk += 4) {
             if (kk >= kr) break;
             double af[2], bf[4];
 #pragma unroll
-            for (int a = 0; a < 2; ++a) af[a] = al * as[(kk + t4) * la + wm + a * 8 + g];
+            for (int a = 0; a < 2; ++a) af[a] = al * as[kcA ? (wm + a * 8 + g) * 20 + kk + t4 : (kk + t4) * 68 + wm + a * 8 + g];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) bf[b] = bs[(kk + t4) * lb + wn + b * 8 + g];
+            for (int b = 0; b < 4; ++b) bf[b] = bs[kcB ? (wn + b * 8 + g) * 20 + kk + t4 : (kk + t4) * 68 + wn + b * 8 + g];
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -159,7 +161,7 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
                     if (a * 8 < am && b * 8 < bn) dmma_884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
         }
     };
-    if (nch <= GM_NS) {
+    if (nch <= VM_NS) {
         // short sums (the latency-bound tasks on the Cholesky's critical path): every chunk
         // in flight at once, a single wait
         for (int s = 0; s < nch; ++s) issue(s);
@@ -169,14 +171,14 @@ __device__ __forceinline__ void vm_mgemm(double* T0, const VTerm* __restrict__ t
         for (int s = 0; s < nch; ++s) compute(s);
     } else {
 #pragma unroll
-        for (int s = 0; s < GM_NS - 1; ++s) {
+        for (int s = 0; s < VM_NS - 1; ++s) {
             issue(s);
             cp_async_commit();
         }
         for (int s = 0; s < nch; ++s) {
-            cp_async_wait<GM_NS - 2>();
+            cp_async_wait<VM_NS - 2>();
             __syncthreads();
-            if (s + GM_NS - 1 < nch) issue(s + GM_NS - 1);
+            if (s + VM_NS - 1 < nch) issue(s + VM_NS - 1);
             cp_async_commit();
             compute(s);
         }
@@ -243,13 +245,13 @@ __device__ __forceinline__ void vm_run(const VTask task, const VIns* __restrict_
                 __syncthreads();
             } break;
             case VM_MGEMM: {
-                const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;   // staging: the other tiles
-                vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by);
+                vm_mgemm(T0, terms + I.goff, I.ld, pool, ranks, sm + NTILE * TSZ, sm + NTILE * TSZ + VM_NS * VM_STAGE,
+                         c_fl, c_by);
             } break;
             case VM_MGEMM_ST: {
-                const int o1 = (I.t0 == 0) ? 1 : 0, o2 = (I.t0 == 2) ? 1 : 2;
                 const int r = dim_eval(I.rows, ranks), c = dim_eval(I.cols, ranks);
-                vm_mgemm(T0, terms + I.pad2, I.t1, pool, ranks, sm + o1 * TSZ, sm + o2 * TSZ, c_fl, c_by, pool + I.goff,
+                vm_mgemm(T0, terms + I.pad2, I.t1, pool, ranks, sm + NTILE * TSZ, sm + NTILE * TSZ + VM_NS * VM_STAGE,
+                         c_fl, c_by, pool + I.goff,
                          I.ld, r, c, I.beta, task.ins_count == 1 ? stt : nullptr);
             } break;
             case VM_ADD: {
