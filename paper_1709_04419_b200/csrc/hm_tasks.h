@@ -103,8 +103,16 @@ constexpr int TR_EXACT_MMAX = 512;   // ... on blocks with at most this many row
                                      // single-CTA Householder QR of a taller factor is HBM-latency
                                      // bound (~25 ms at 8192 x 160); those take the cooperative
                                      // randomized path instead
+// narrow stacks (static width <= 64, e.g. the recompression of an ACA factor) take the
+// exact path on blocks up to TR_EXACT_MN rows: its K column steps beat the randomized
+// path's ~40 latency-bound stages
+#ifndef HM_TR_EXACT_MN
+#define HM_TR_EXACT_MN 512
+#endif
+constexpr int TR_EXACT_MN = HM_TR_EXACT_MN;
 HM_HD inline bool trunc_exact_path(int32_t m, int32_t q, int32_t kmax_tot) {
-    return kmax_tot <= TR_EXACT_K && m <= TR_EXACT_MMAX && q <= TR_EXACT_MMAX;
+    return (kmax_tot <= TR_EXACT_K && m <= TR_EXACT_MMAX && q <= TR_EXACT_MMAX) ||
+           (kmax_tot <= 64 && m <= TR_EXACT_MN && q <= TR_EXACT_MN);
 }
 constexpr int TR_RB = 16;         // probes per block of the randomized range finder
 #ifndef HM_TR_NB

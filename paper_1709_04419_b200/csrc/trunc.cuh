@@ -45,6 +45,9 @@ constexpr int TR_THREADS = 256;
 // (sigma_i > |eps| = eps * sigma^2, the default: the paper's Remark 2 wording, reading R4)
 __device__ __forceinline__ double tr_cut(double eps, double smax) { return eps > 0.0 ? eps * smax : -eps; }
 constexpr int ORDER_MAX = 512;
+// exact path in shared memory: behind `order` (ORDER_MAX ints), up to TR_XS_DOUBLES doubles
+constexpr int TR_XS_OFF = ORDER_MAX / 2;
+constexpr int TR_XS_DOUBLES = 22016;              // 172 KB: e.g. 256 + 256 rows x K = 36
 // Range-finder stopping rule.  For a Gaussian probe w, E ||R w||^2 = ||R||_F^2, so
 // the probe norms ||M w_j|| estimate ||M||_F and the projected-probe norms
 // ||(I - Q Q^T) M w_j|| estimate ||M - Q Q^T M||_F.  The basis is complete when
@@ -63,51 +66,70 @@ constexpr double TR_GRAM_EPS = 1e-7;
 // dynamic shared memory: [Cs (leader) | staging] then order, koff
 constexpr int TR_SMEM_A = 8 * GEMM_SMEM_DOUBLES;   // GEMM staging, then order / koff
 
-// Householder QR of A (m x K, ld m) in place; tau[K].  R in the upper triangle.
-static __device__ __noinline__ void house_qr(double* A, int m, int K, double* tau, double* scratch) {
+// Householder QR of A (m x K, ld m) in place; tau[K].  R in the upper triangle, the
+// reflectors v (v_i = 1 implicit) below it.  Two CTA barriers per column: the
+// reflector is applied in its unscaled form (the scale 1 / (alpha - beta) folded
+// into w), the warp that updates column i + 1 also forms that column's norm below
+// the diagonal for the next step, and the reflectors are scaled in one pass at the end.
+// sc: K doubles of scratch (shared memory preferred).
+static __device__ __noinline__ void house_qr(double* A, int m, int K, double* tau, double* sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int kmin = min(m, K);
-    __shared__ double s_beta, s_scale, s_tau;
+    __shared__ double s_sig, s_tau, s_sc;
+    if (warp == 0) {                                   // norm of column 0 below the diagonal
+        double ss = 0.0;
+        for (int r = 1 + lane; r < m; r += 32) ss += A[r] * A[r];
+        ss = warp_sum(ss);
+        if (lane == 0) s_sig = ss;
+    }
+    __syncthreads();
     for (int i = 0; i < kmin; ++i) {
         double* a = A + (int64_t)i * m;
-        double ss = 0.0;
-        for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) ss += a[r] * a[r];
-        const double sig = block_sum(ss, scratch);
         if (threadIdx.x == 0) {
-            const double alpha = a[i];
+            const double alpha = a[i], sig = s_sig;
             if (sig == 0.0) {
                 s_tau = 0.0;
-                s_scale = 0.0;
-                s_beta = alpha;
+                s_sc = 0.0;
             } else {
                 const double nrm = sqrt(alpha * alpha + sig);
                 const double beta = (alpha <= 0.0) ? nrm : -nrm;
                 s_tau = (beta - alpha) / beta;
-                s_scale = 1.0 / (alpha - beta);
-                s_beta = beta;
+                s_sc = 1.0 / (alpha - beta);
+                a[i] = beta;
             }
             tau[i] = s_tau;
+            sc[i] = s_sc;
+            s_sig = 0.0;
         }
         __syncthreads();
-        const double tv = s_tau, sc = s_scale;
-        if (tv != 0.0)
-            for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) a[r] *= sc;
-        __syncthreads();
-        if (threadIdx.x == 0) a[i] = s_beta;
-        __syncthreads();
-        if (tv != 0.0) {
-            // apply H = I - tau v v^T (v_i = 1) to columns c > i: one warp per column
-            for (int c = i + 1 + warp; c < K; c += nw) {
-                double* col = A + (int64_t)c * m;
-                double w = (lane == 0) ? col[i] : 0.0;
+        const double tv = s_tau, scl = s_sc;
+        // apply H = I - tau v v^T (v_i = 1, v_r = scl a_r) to columns c > i: one warp per column
+        for (int c = i + 1 + warp; c < K; c += nw) {
+            double* col = A + (int64_t)c * m;
+            if (tv != 0.0) {
+                double w = 0.0;
                 for (int r = i + 1 + lane; r < m; r += 32) w += a[r] * col[r];
-                w = warp_sum(w) * tv;
+                w = (warp_sum(w) * scl + col[i]) * tv;
                 if (lane == 0) col[i] -= w;
-                for (int r = i + 1 + lane; r < m; r += 32) col[r] -= w * a[r];
+                const double ws = w * scl;
+                for (int r = i + 1 + lane; r < m; r += 32) col[r] -= ws * a[r];
+            }
+            if (c == i + 1) {                          // next column's norm below its diagonal
+                __syncwarp();
+                double ss = 0.0;
+                for (int r = i + 2 + lane; r < m; r += 32) ss += col[r] * col[r];
+                ss = warp_sum(ss);
+                if (lane == 0) s_sig = ss;
             }
         }
         __syncthreads();
     }
+    for (int i = warp; i < kmin; i += nw) {            // scale the reflectors
+        double* a = A + (int64_t)i * m;
+        const double scl = sc[i];
+        for (int r = i + 1 + lane; r < m; r += 32) a[r] *= scl;
+    }
+    __syncthreads();
 }
 
 // Y (m x r, ld m) <- Q Y with Q = H_0 H_1 ... H_{kmin-1} stored in A (m x K) / tau
@@ -205,11 +227,16 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
                             int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
                             double* dsm) {
     __shared__ double scratch[32];
+    __shared__ double s_hsc[TR_EXACT_K];           // Householder scales
     int* order = (int*)dsm;                        // ORDER_MAX ints (dynamic shared memory)
     __shared__ int s_flag;
     __shared__ int s_rank;
     const int m = t.m, q = t.q;
-    double* ws = pool + t.ws;
+    // the stacks, cores and factors live in shared memory when they fit (the column-serial
+    // QR and the Jacobi sweeps are latency-bound: global memory made them several times
+    // slower), else in the task's global workspace
+    const bool insm = (int64_t)(m + q + 3) * K + 2 * (int64_t)K * K <= TR_XS_DOUBLES;
+    double* ws = insm ? dsm + TR_XS_OFF : pool + t.ws;
     double* A = ws;                       // m x K
     double* Bm = A + (int64_t)m * K;      // q x K
     double* tauA = Bm + (int64_t)q * K;   // K
@@ -241,8 +268,8 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
         if (threadIdx.x == 0) ranks[t.rslot] = 0;
         return;
     }
-    house_qr(A, m, K, tauA, scratch);
-    house_qr(Bm, q, K, tauB, scratch);
+    house_qr(A, m, K, tauA, s_hsc);
+    house_qr(Bm, q, K, tauB, s_hsc);
     const int Ka = min(m, K), Kb = min(q, K);
     // X = R_A R_B^T  (Ka x Kb), R_A[i][c] (c >= i) = A[i + c m], R_B[j][c] = Bm[j + c q]
     for (int idx = threadIdx.x; idx < Ka * Kb; idx += blockDim.x) {
@@ -254,7 +281,8 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
     __syncthreads();
     // the small SVD is latency-bound: staged in shared memory behind `order` when it fits
     // (Ka x Kb + Kb x Kb doubles, i.e. K <= 68; global memory made it ~10x slower)
-    jacobi_smem(X, Ka, Kb, Z, dsm + ORDER_MAX / 2, &s_flag);
+    if (insm) jacobi_svd(X, Ka, Kb, Z, &s_flag);
+    else jacobi_smem(X, Ka, Kb, Z, dsm + ORDER_MAX / 2, &s_flag);
     // singular values = column norms of X
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = warp; j < Kb; j += nw) {
@@ -937,7 +965,7 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
             // ---- F3 (Householder path): QR of a copy of W, S = R^T, Jacobi S Z = X'
             for (int idx = threadIdx.x; idx < q * ell; idx += blockDim.x) W.Wc[idx] = W.Wm[idx];
             __syncthreads();
-            house_qr(W.Wc, q, ell, W.tau, scratch);
+            house_qr(W.Wc, q, ell, W.tau, W.sig);   // (sig: scratch here, filled below)
             for (int idx = threadIdx.x; idx < ell * Kw; idx += blockDim.x) {
                 const int i = idx % ell, j = idx / ell;
                 W.S[i + (int64_t)j * ell] = (i >= j) ? W.Wc[j + (int64_t)i * q] : 0.0;
@@ -1009,7 +1037,9 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
 }
 
 // dynamic shared memory (bytes) the truncation needs
-constexpr int TR_SMEM = TR_SMEM_A + ORDER_MAX * 4 + (TR_PMAX + 1) * 4;
+constexpr int TR_SMEM_R = TR_SMEM_A + ORDER_MAX * 4 + (TR_PMAX + 1) * 4;
+constexpr int TR_SMEM_X = TR_XS_OFF * 8 + TR_XS_DOUBLES * 8;
+constexpr int TR_SMEM = TR_SMEM_R > TR_SMEM_X ? TR_SMEM_R : TR_SMEM_X;
 
 // sub / nsub / bar: this CTA's index in a cooperative truncation (nsub CTAs,
 // persistent executor only), else 0 / 1 / nullptr
