@@ -151,9 +151,17 @@ static __device__ __noinline__ void house_apply_q(const double* A, int m, int km
     }
 }
 
-// one-sided Jacobi: X (rows x n, ld rows) -> X Z with orthogonal columns; Z (n x n, ld n)
+// one-sided Jacobi: X (rows x n, ld rows) -> X Z with orthogonal columns; Z (n x n, ld n).
+// Round-robin pairing, one pair per half-warp (16 lanes stride the rows), so a round of
+// up to 16 pairs is one pass of the 8 warps; the half-warp sums use 4 shuffle levels.
+__device__ __forceinline__ double half_sum(double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 static __device__ __noinline__ void jacobi_svd(double* X, int rows, int n, double* Z, int* s_flag) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int hl = lane & 15, half = lane >> 4;
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Z[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
     __syncthreads();
     if (n < 2) return;
@@ -162,38 +170,41 @@ static __device__ __noinline__ void jacobi_svd(double* X, int rows, int n, doubl
         if (threadIdx.x == 0) *s_flag = 0;
         __syncthreads();
         for (int round = 0; round < nn - 1; ++round) {
-            for (int pr = warp; pr < nn / 2; pr += nw) {
+            // all lanes of a warp take the same number of steps (the shuffles need both halves)
+            for (int base = 2 * warp; base < nn / 2; base += 2 * nw) {
+                const int pr = base + half;
                 // round-robin pairing: player 0 fixed, others rotate
                 int a = (pr == 0) ? 0 : ((round + pr - 1) % (nn - 1)) + 1;
                 int b = ((round + nn - 2 - pr) % (nn - 1)) + 1;
                 if (pr == 0) b = ((round + nn - 2) % (nn - 1)) + 1;
-                if (a >= n || b >= n) continue;
+                const bool act = pr < nn / 2 && a < n && b < n;
                 if (a > b) { int tmp = a; a = b; b = tmp; }
-                double* xa = X + (int64_t)a * rows;
-                double* xb = X + (int64_t)b * rows;
+                double* xa = X + (int64_t)(act ? a : 0) * rows;
+                double* xb = X + (int64_t)(act ? b : 0) * rows;
                 double al = 0.0, be = 0.0, ga = 0.0;
-                for (int r = lane; r < rows; r += 32) {
-                    const double u = xa[r], v = xb[r];
-                    al += u * u; be += v * v; ga += u * v;
-                }
-                al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-                if (fabs(ga) > 1e-14 * sqrt(al * be) && ga != 0.0) {
+                if (act)
+                    for (int r = hl; r < rows; r += 16) {
+                        const double u = xa[r], v = xb[r];
+                        al += u * u; be += v * v; ga += u * v;
+                    }
+                al = half_sum(al); be = half_sum(be); ga = half_sum(ga);
+                if (act && fabs(ga) > 1e-14 * sqrt(al * be) && ga != 0.0) {
                     const double zeta = (be - al) / (2.0 * ga);
                     const double tt = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-                    for (int r = lane; r < rows; r += 32) {
+                    for (int r = hl; r < rows; r += 16) {
                         const double u = xa[r], v = xb[r];
                         xa[r] = c * u - s * v;
                         xb[r] = s * u + c * v;
                     }
                     double* za = Z + (int64_t)a * n;
                     double* zb = Z + (int64_t)b * n;
-                    for (int r = lane; r < n; r += 32) {
+                    for (int r = hl; r < n; r += 16) {
                         const double u = za[r], v = zb[r];
                         za[r] = c * u - s * v;
                         zb[r] = s * u + c * v;
                     }
-                    if (lane == 0) *s_flag = 1;
+                    if (hl == 0) *s_flag = 1;
                 }
             }
             __syncthreads();
