@@ -10,6 +10,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -56,16 +57,21 @@ def build(verbose: bool = False) -> str:
             os.remove(o)
         with open(stamp, "w") as f:
             f.write(defs)
+    jobs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
         if _newer(src, obj):
-            _run([NVCC, *NVCC_FLAGS, "-c", src, "-o", obj], log)
+            jobs.append([NVCC, *NVCC_FLAGS, "-c", src, "-o", obj])
         objs.append(obj)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
         if _newer(src, obj):
-            _run(["g++", *CXX_FLAGS, "-c", src, "-o", obj], log)
+            jobs.append(["g++", *CXX_FLAGS, "-c", src, "-o", obj])
         objs.append(obj)
+    # translation units compile independently: one process per unit
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, cmd, log) for cmd in jobs]:
+            f.result()
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
               "-lcudart"], log)

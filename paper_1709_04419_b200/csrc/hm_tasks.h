@@ -114,7 +114,12 @@ HM_HD inline bool trunc_exact_path(int32_t m, int32_t q, int32_t kmax_tot) {
     return (kmax_tot <= TR_EXACT_K && m <= TR_EXACT_MMAX && q <= TR_EXACT_MMAX) ||
            (kmax_tot <= 64 && m <= TR_EXACT_MN && q <= TR_EXACT_MN);
 }
-constexpr int TR_RB = 16;         // probes per block of the randomized range finder
+#ifndef HM_TR_RB
+#define HM_TR_RB 16
+#endif
+constexpr int TR_RB = HM_TR_RB;   // probes per block of the randomized range finder (<= 32: one
+                                  // warp lane per probe in the pivoted Cholesky)
+static_assert(TR_RB >= 8 && TR_RB <= 32 && TR_RB % 8 == 0, "TR_RB");
 #ifndef HM_TR_NB
 #define HM_TR_NB 4
 #endif
@@ -135,6 +140,7 @@ constexpr int64_t TR_COOP_WORK = int64_t(1) << HM_COOP_WORK_LOG2;   // (m + q) *
 constexpr int TR_COOP_MAX = 32;   // CTAs per cooperative truncation (hard limit; the plan's
                                   // cap hm_params.coop_max defaults to TR_COOP_DEFAULT)
 constexpr int TR_COOP_DEFAULT = 16;
+constexpr unsigned long long TR_COOP_WATCHDOG_NS = 120ull * 1000000000ull;   // group-barrier wait before __trap (trunc.cuh)
 #ifndef HM_TR_SHRINK
 #define HM_TR_SHRINK 1
 #endif

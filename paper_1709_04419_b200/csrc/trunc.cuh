@@ -393,7 +393,14 @@ __device__ __forceinline__ void coop_sync(int* bar, int nsub, int& gen, unsigned
             __threadfence();
             atomicAdd(bar, 1);
             const int target = gen * nsub;
-            while (ld_acquire_gpu(bar) < target) __nanosleep(32);
+            // Liveness rests on the group's CTAs being co-resident (exec.cu); a partner
+            // that never arrives (e.g. other work holding the SMs) traps after
+            // TR_COOP_WATCHDOG_NS instead of hanging: the launch fails, hm_* -> HM_ERR_CUDA.
+            const unsigned long long t0 = gtimer();
+            while (ld_acquire_gpu(bar) < target) {
+                __nanosleep(32);
+                if (gtimer() - t0 > TR_COOP_WATCHDOG_NS) __trap();
+            }
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
         __syncthreads();

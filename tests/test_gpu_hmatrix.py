@@ -315,6 +315,29 @@ def test_loglik_multi_different_locations(hm):
         hm._binding.check(rc)
 
 
+def test_rank_cap_is_an_error_not_a_truncation(hm, config0):
+    """A rank above the block capacity is HM_ERR_RANK_CAP (include/hmlik.h:52), never a silent
+    truncation below eps (Remark 2, l.166): configs[0] points at eps = 1e-10 need ranks far
+    above kmax = 4 (assembly); at kmax = 12 and eps = 1e-8 the assembly fits (max rank of C~
+    is checked) but the factor's fill-in does not, or the factor fits and is then exact."""
+    pts, theta, Z, (oll, old, oq) = config0
+    with pytest.raises(hm.HMError) as e:
+        H = hm.HMatrix(pts, theta, eps=1e-10, leaf=32, eta=2.0, kmax=4)
+        H.cholesky()
+    assert e.value.code == -4
+    for kmax in (8, 12, 16):
+        try:
+            H = hm.HMatrix(pts, theta, eps=1e-8, leaf=32, eta=2.0, kmax=kmax)
+            H.cholesky()
+        except hm.HMError as err:
+            assert err.code == -4
+            continue
+        st = H.stats()
+        assert st["max_rank_C"] <= kmax and st["max_rank_L"] <= kmax
+        got = H.loglik(Z)[0, 0]
+        assert abs(got - oll) / abs(oll) <= 1e-6
+
+
 @pytest.mark.parametrize("scale", [1.0, 0.25])
 def test_adaptive_capacities(hm, config0, monkeypatch, scale):
     """hm_params.adaptive_cap: rank capacities sized per block from the assembled C~'s ranks
