@@ -234,6 +234,33 @@ static __device__ __forceinline__ void jacobi_smem(double* X, int rows, int n, d
 }
 
 // ---------------------------------------------------------------- exact path
+// dst (len x w, ld len) = al * rows [row0, row0 + rows) of the piece src (ld sld), zero
+// elsewhere.  The element loop is batched 8 deep (all loads, then all stores): one
+// load in flight per thread made the gathers latency-bound.  Pieces are written by
+// other CTAs of the persistent executor: read through L2.
+__device__ __forceinline__ void gather_cols(double* __restrict__ dst, int len, const double* __restrict__ src,
+                                            int64_t sld, int row0, int rows, int w, double al) {
+    const int tot = len * w;                       // exact path: len <= TR_EXACT_MMAX, w <= K
+    for (int base = threadIdx.x; base < tot; base += 8 * blockDim.x) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * blockDim.x;
+            v[u] = 0.0;
+            if (idx < tot) {
+                const int r = idx % len, c = idx / len;
+                const int rr = r - row0;
+                if (rr >= 0 && rr < rows) v[u] = al * __ldcg(src + rr + (int64_t)c * sld);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * blockDim.x;
+            if (idx < tot) dst[idx] = v[u];
+        }
+    }
+}
+
 static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restrict__ pieces, double* __restrict__ pool,
                             int* __restrict__ ranks, int* __restrict__ flags, double eps, double* __restrict__ ctr,
                             double* dsm) {
@@ -262,16 +289,8 @@ static __device__ void trunc_exact(const TTask& t, int K, const TPiece* __restri
         const int w = dim_eval(pc.w, ranks);
         const double* Up = pool + pc.u_off;
         const double* Vp = pool + pc.v_off;
-        for (int idx = threadIdx.x; idx < m * w; idx += blockDim.x) {
-            const int r = idx % m, c = idx / m;
-            const int rr = r - pc.u_row0;
-            A[(int64_t)(koff + c) * m + r] = (rr >= 0 && rr < pc.u_rows) ? pc.alpha * Up[rr + (int64_t)c * pc.u_ld] : 0.0;
-        }
-        for (int idx = threadIdx.x; idx < q * w; idx += blockDim.x) {
-            const int r = idx % q, c = idx / q;
-            const int rr = r - pc.v_row0;
-            Bm[(int64_t)(koff + c) * q + r] = (rr >= 0 && rr < pc.v_rows) ? Vp[rr + (int64_t)c * pc.v_ld] : 0.0;
-        }
+        gather_cols(A + (int64_t)koff * m, m, Up, pc.u_ld, pc.u_row0, pc.u_rows, w, pc.alpha);
+        gather_cols(Bm + (int64_t)koff * q, q, Vp, pc.v_ld, pc.v_row0, pc.v_rows, w, 1.0);
         koff += w;
     }
     __syncthreads();
@@ -648,32 +667,54 @@ static __device__ void trunc_rand(const TTask& t, int K, const TPiece* __restric
     }
     __syncthreads();
     // gather the stacks A = [alpha_p pad(U_p)] (m x K) and B = [pad(V_p)] (q x K): one warp per
-    // (stacked column, 256-row block) item, 8 independent loads per lane, coalesced
+    // (stacked column, 256-row block) item, 8 loads per lane, coalesced; GB items per warp in
+    // flight (all loads, then all stores: one item at a time left the gather latency-bound)
     {
+        constexpr int GB = 4;
         const int rbm = (m + 255) / 256, rbq = (q + 255) / 256;
         const int64_t nitem = (int64_t)K * (rbm + rbq);
-        for (int64_t it = (int64_t)sub * nw + warp; it < nitem; it += (int64_t)nsub * nw) {
-            const int k = (int)(it / (rbm + rbq)), rb = (int)(it % (rbm + rbq));
-            const int p = piece_of(koff, np, k);
-            const TPiece& pc = pieces[t.piece_begin + p];
-            const int c = k - koff[p];
-            const bool isu = rb < rbm;
-            const int r0 = (isu ? rb : rb - rbm) * 256;
-            const int nr = isu ? m : q;
-            const int row0 = isu ? pc.u_row0 : pc.v_row0, rows = isu ? pc.u_rows : pc.v_rows;
-            const double al = isu ? pc.alpha : 1.0;
-            const double* src = pool + (isu ? pc.u_off + (int64_t)c * pc.u_ld : pc.v_off + (int64_t)c * pc.v_ld);
-            double* dst = isu ? W.Ast + (int64_t)k * m : W.Bst + (int64_t)k * q;
-            double v[8];
+        const int64_t wstride = (int64_t)nsub * nw;
+        for (int64_t it0 = (int64_t)sub * nw + warp; it0 < nitem; it0 += GB * wstride) {
+            double v[GB][8];
+            double* dsts[GB];
+            int r0s[GB], nrs[GB];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = r0 + lane + 32 * u, ii = i - row0;
-                v[u] = (i < nr && ii >= 0 && ii < rows) ? al * __ldcg(src + ii) : 0.0;
+            for (int b2 = 0; b2 < GB; ++b2) {
+                const int64_t it = it0 + b2 * wstride;
+                dsts[b2] = nullptr;
+                r0s[b2] = 0;
+                nrs[b2] = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[b2][u] = 0.0;
+                if (it < nitem) {
+                    const int k = (int)(it / (rbm + rbq)), rb = (int)(it % (rbm + rbq));
+                    const int p = piece_of(koff, np, k);
+                    const TPiece& pc = pieces[t.piece_begin + p];
+                    const int c = k - koff[p];
+                    const bool isu = rb < rbm;
+                    const int r0 = (isu ? rb : rb - rbm) * 256;
+                    const int nr = isu ? m : q;
+                    const int row0 = isu ? pc.u_row0 : pc.v_row0, rows = isu ? pc.u_rows : pc.v_rows;
+                    const double al = isu ? pc.alpha : 1.0;
+                    const double* src = pool + (isu ? pc.u_off + (int64_t)c * pc.u_ld : pc.v_off + (int64_t)c * pc.v_ld);
+                    dsts[b2] = isu ? W.Ast + (int64_t)k * m : W.Bst + (int64_t)k * q;
+                    r0s[b2] = r0;
+                    nrs[b2] = nr;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int i = r0 + lane + 32 * u, ii = i - row0;
+                        if (i < nr && ii >= 0 && ii < rows) v[b2][u] = al * __ldcg(src + ii);
+                    }
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = r0 + lane + 32 * u;
-                if (i < nr) dst[i] = v[u];
+            for (int b2 = 0; b2 < GB; ++b2) {
+                if (dsts[b2] == nullptr) continue;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = r0s[b2] + lane + 32 * u;
+                    if (i < nrs[b2]) dsts[b2][i] = v[b2][u];
+                }
             }
         }
     }
