@@ -115,18 +115,21 @@ HM_HD inline bool trunc_exact_path(int32_t m, int32_t q, int32_t kmax_tot) {
            (kmax_tot <= 64 && m <= TR_EXACT_MN && q <= TR_EXACT_MN);
 }
 #ifndef HM_TR_RB
-#define HM_TR_RB 16
+#define HM_TR_RB 8
 #endif
 constexpr int TR_RB = HM_TR_RB;   // probes per block of the randomized range finder (<= 32: one
                                   // warp lane per probe in the pivoted Cholesky)
 static_assert(TR_RB >= 8 && TR_RB <= 32 && TR_RB % 8 == 0, "TR_RB");
 #ifndef HM_TR_NB
-#define HM_TR_NB 4
+#define HM_TR_NB 8
 #endif
-constexpr int TR_NB = HM_TR_NB;   // blocks per pass over the stacks: 4 x 16 = 64 probes fill the
-                                  // 64-wide GEMM tiles exactly and resolve ranks up to ~48 in one pass
+constexpr int TR_NB = HM_TR_NB;   // blocks per pass over the stacks: 8 x 8 = 64 probes fill the
+                                  // 64-wide GEMM tiles exactly and resolve ranks up to ~56 in one pass
+                                  // (measured at n = 64k: 8 x 8 7.27 evals/s, 4 x 16 6.91, 2 x 32 5.50)
 constexpr int TR_PW = TR_RB * TR_NB;
-constexpr int TR_LMAX = 256;      // max basis width cap + RB  (so kmax <= 240)
+constexpr int TR_LMAX = 256;      // max basis width cap + RB
+constexpr int HM_KMAX_LIMIT = 240;   // hm_params.kmax bound (include/hmlik.h)
+static_assert(HM_KMAX_LIMIT <= TR_LMAX - TR_RB, "kmax limit");
 constexpr int TR_RCH = 64;        // fixed row chunk of the cooperative truncation (8 warps x 8 rows)
 constexpr int TR_TCH = 128;       // stacked columns staged per shared-memory chunk
 constexpr int TR_PMAX = 1023;     // pieces per truncation

@@ -566,7 +566,7 @@ int hm_build(const double* locs, int32_t locs_on_device, int64_t n, hm_theta the
         if (params.kmax <= 0) params.kmax = 160;
         if (params.coop_max <= 0) params.coop_max = TR_COOP_DEFAULT;
         if (params.coop_max > TR_COOP_MAX) throw ApiError(HM_ERR_ARG, "coop_max <= 32 required");
-        if (params.kmax > TR_LMAX - TR_RB) throw ApiError(HM_ERR_ARG, "kmax <= 240 required");
+        if (params.kmax > HM_KMAX_LIMIT) throw ApiError(HM_ERR_ARG, "kmax <= 240 required");
         if (params.exec_ctas < 0) throw ApiError(HM_ERR_ARG, "exec_ctas >= 0 required");
         if (params.adaptive_cap < 0 || params.adaptive_cap > 1) throw ApiError(HM_ERR_ARG, "adaptive_cap must be 0 or 1");
         check_theta(theta);

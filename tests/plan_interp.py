@@ -344,7 +344,7 @@ class InterpRand(Interp):
     eps * max_j ||M w_j|| (relative Frobenius certificate), then
     W = M^T Q, QR, SVD of R^T,
     U = Q X', V = W X' Sigma^-2.  Used to check that algorithm on the CPU."""
-    RB = 16
+    RB = 8             # hm_tasks.h TR_RB
     EXACT_K = 160      # hm_tasks.h TR_EXACT_K / TR_EXACT_MMAX (trunc_exact_path)
     EXACT_MMAX = 512
 
