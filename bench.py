@@ -369,6 +369,8 @@ def run_gpu(args, w):
     # cooperative groups <= 8 CTAs when co-scheduled, and within the deadlock bound
     # 4 * (coop - 1) < executor CTAs = sms / S
     coop = 16 if S == 1 else max(1, min(8, (sms // S - 1) // 4 + 1))
+    if args.coop_max > 0:
+        coop = min(args.coop_max, (sms // S - 1) // 4 + 1)
     kmax = w.get("kmax", args.kmax)
     pts = make_points(w)
     n = pts.shape[0]
@@ -531,6 +533,8 @@ def main():
     ap.add_argument("--replicates", type=int, default=0,
                     help="--workload mc: replicates in the timed region (0 = gpus * steps * theta-streams; "
                          "configs[3] is 128)")
+    ap.add_argument("--coop-max", type=int, default=0,
+                    help="cap of cooperative truncation groups (0 = 16 at S = 1, else min(8, deadlock bound))")
     ap.add_argument("--theta-streams", type=int, default=4,
                     help="independent theta evaluations co-scheduled per GPU (1 = single-evaluation latency)")
     args = ap.parse_args()
